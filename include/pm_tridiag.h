@@ -1,0 +1,172 @@
+/*
+ * pm_tridiag.h -- C ABI of the B200-native partition-method tridiagonal solver.
+ *
+ * Drop-in boundary.  The reference ships no solver
+ * (/root/reference/SPEC.md:12 puts "the CUDA solver itself" out of scope);
+ * its only code is the header-only streamtune API
+ * (/root/reference/proj/include/streamtune/timing_model.hpp,
+ *  /root/reference/proj/include/streamtune/errors.hpp).  The north_star
+ * names the solver API the paper's C++ code exposes: "coefficient arrays
+ * a/b/c/d in, x out, sub-system size m, num_streams" (PAPER.md:52 m = 10,
+ * FP64; PAPER.md:54-60 streams are powers of two up to 32).  This header is
+ * that API as a plain C ABI (no torch types, no exceptions):
+ *
+ *   pm_solve_host_f64    <- the paper's whole pipeline:
+ *                           host a,b,c,d -> x with H2D / kernels / D2H
+ *                           overlapped over num_streams CUDA streams;
+ *                           num_streams == 0 asks the streamtune predictor
+ *                           (SPEC.md:267 recommend) for the count.
+ *   pm_solve_device_f64  <- Stages 1-3 on device-resident arrays
+ *                           (PAPER.md:80 Stage 1 / Stage 3 kernels; Stage 2
+ *                           runs on the GPU here instead of PAPER.md:63's CPU).
+ *   pm_solve_batch_device_f64, pm_dist_*  <- B200 additions (BASELINE.json
+ *                           configs 4 and 5).
+ *   pm_recommend_streams <- streamtune::recommend.
+ *
+ * Conventions
+ *   - a: sub-diagonal, b: diagonal, c: super-diagonal, d: right-hand side,
+ *     all length n; a[0] and c[n-1] are ignored (treated as 0).  x may alias d.
+ *   - 2 <= m <= PM_MAX_M.  Sub-system size of Stage 1.
+ *   - The caller owns every buffer; the library never frees caller memory.
+ *   - Status codes: PM_OK; PM_ERR_VALIDATION (streamtune::ValidationError,
+ *     errors.hpp:9-14: n < 1, m out of range, bad stream count -- the
+ *     InvalidStreamCountError of errors.hpp:75-86 --, null pointers);
+ *     PM_ERR_COMPUTATION (streamtune::ComputationError, errors.hpp:16-21:
+ *     zero or non-finite pivot); PM_ERR_RUNTIME (CUDA / NCCL failure).
+ *     The message is in pm_last_error(h).
+ *   - A handle is single-threaded: one handle per host thread / per GPU.
+ *   - Systems must be solvable without pivoting (e.g. diagonally dominant),
+ *     as for the paper's method.
+ */
+#ifndef PM_TRIDIAG_H
+#define PM_TRIDIAG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PM_OK 0
+#define PM_ERR_VALIDATION 1
+#define PM_ERR_COMPUTATION 2
+#define PM_ERR_RUNTIME 3
+
+#define PM_MAX_M 128
+
+typedef struct pm_handle_s* pm_handle_t;
+
+/* Mirrors streamtune::StageTimings (timing_model.hpp:77-85).  ms. */
+typedef struct pm_stage_timings {
+  uint64_t slae_size;
+  double t1_h2d, t1_comp, t1_d2h, t2_comp, t3_h2d, t3_comp, t3_d2h;
+} pm_stage_timings;
+
+/* Mirrors streamtune::ModelBundle. */
+typedef struct pm_model_bundle {
+  double sum_a, sum_b;
+  double small_a, small_b, small_c;
+  double big_a, big_b, big_c;
+  uint64_t size_threshold;
+  int32_t num_candidates;
+  int32_t candidates[5];
+} pm_model_bundle;
+
+/* Options for pm_set_option. */
+#define PM_OPT_STAGES 1        /* bulk-copy ring depth per CTA, 1..4 (default 2)   */
+#define PM_OPT_STREAM_MODE 2   /* 0: pooled streams (default); 1: create and destroy
+                                  the streams inside every solve, as the paper's
+                                  T_overhead measures      */
+#define PM_OPT_REVERSE_SOLVE 3 /* 1 (default): Stage 3 walks tiles last-to-first so
+                                  the tail Stage 1 left in L2 is re-read from L2   */
+#define PM_OPT_MAX_CTAS 4      /* cap on persistent CTAs per launch (0 = none)     */
+#define PM_OPT_TIMINGS 5       /* 1: record StageTimings with CUDA events in
+                                  pm_solve_host_f64 (num_streams == 1 only)        */
+#define PM_OPT_KERNEL_TIMES 6  /* 1: bracket every kernel launch with CUDA events;
+                                  read them with pm_kernel_times                   */
+
+int pm_create(pm_handle_t* out, int device);
+int pm_destroy(pm_handle_t h);
+const char* pm_last_error(pm_handle_t h);
+int pm_set_option(pm_handle_t h, int option, int64_t value);
+int pm_get_version(void); /* major*10000 + minor*100 + patch */
+
+/* Device-resident solve (stream-ordered, asynchronous; stream NULL = default
+ * stream).  Pivot failures are reported by the next pm_check(). */
+int pm_solve_device_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                        const double* d, double* x, int64_t n, int32_t m, void* stream);
+
+/* Batch of independent systems stored back to back (system k occupies rows
+ * [k*n_per_system, (k+1)*n_per_system)); each system's first a and last c
+ * are ignored.  Asynchronous like pm_solve_device_f64. */
+int pm_solve_batch_device_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                              const double* d, double* x, int64_t n_per_system, int64_t batch,
+                              int32_t m, void* stream);
+
+/* Waits for the handle's last stream; PM_ERR_COMPUTATION if any solve since
+ * the previous check met a zero or non-finite pivot (the flag is cleared). */
+int pm_check(pm_handle_t h);
+
+/* End-to-end solve from host memory (synchronous).  num_streams in
+ * {0, 1, 2, 4, 8, 16, 32}; 0 = predictor.  Page-locked buffers (cudaHostAlloc
+ * or pm_host_register) are required for copy/compute overlap. */
+int pm_solve_host_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                      const double* d, double* x, int64_t n, int32_t m, int32_t num_streams);
+
+/* StageTimings of the last pm_solve_host_f64 (components are filled when it
+ * ran with one stream and PM_OPT_TIMINGS=1), its total time and stream count. */
+int pm_last_stage_timings(pm_handle_t h, pm_stage_timings* out, double* total_ms,
+                          int32_t* streams_used);
+
+int pm_host_register(void* ptr, uint64_t bytes);
+int pm_host_unregister(void* ptr);
+
+/* Stream-count model used when num_streams == 0. */
+int pm_set_model_bundle(pm_handle_t h, const pm_model_bundle* bundle);
+int pm_get_model_bundle(pm_handle_t h, pm_model_bundle* out);
+/* streamtune::recommend; bundle NULL = the paper's RTX 2080 Ti bundle.
+ * Returns the stream count (>= 1) or -1 on a validation error. */
+int pm_recommend_streams(int64_t n, const pm_model_bundle* bundle);
+int pm_paper_bundle(pm_model_bundle* out);
+
+/* Counter-based synthetic system (bit-identical to the CPU oracle's
+ * generator): a, c ~ U(-1,1) with a[0] = c[n-1] = 0, b = +-(|a|+|c|+1+U(0,1)),
+ * d ~ U(-1,1).  Any output may be NULL. */
+int pm_generate_f64(pm_handle_t h, double* a, double* b, double* c, double* d, int64_t n,
+                    uint64_t seed, void* stream);
+/* Rows [row0, row0 + count) of the same n_total-row system, written to
+ * a[0..count) etc. (a rank's slice of a row-sharded system). */
+int pm_generate_range_f64(pm_handle_t h, double* a, double* b, double* c, double* d,
+                          int64_t n_total, int64_t row0, int64_t count, uint64_t seed,
+                          void* stream);
+
+/* Row-sharded single system over `world` ranks (BASELINE.json config 5).
+ * Rank r holds rows [offset_r, offset_r + n_local) in a,b,c,d.
+ *   1. pm_dist_reduce_f64: Stage 1 + local levels; writes the rank's two
+ *      interface equations (8 doubles) to iface (device memory).
+ *   2. caller all-gathers iface over ranks into iface_all (8*world doubles,
+ *      rank order), e.g. ncclAllGather / torch.distributed.
+ *   3. pm_dist_solve_f64: solves the 2*world-row interface system
+ *      redundantly, then Stages 3 of all local levels; writes x.
+ * Both calls are asynchronous on `stream` and must use the same n_local, m. */
+int pm_dist_reduce_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                       const double* d, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                       double* iface, void* stream);
+int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                      const double* d, double* x, int64_t n_local, int32_t m, int32_t rank,
+                      int32_t world, const double* iface_all, void* stream);
+
+/* Diagnostics: number of kernel launches the last solve call enqueued, and
+ * the level plan (rows per level) of the last plan. */
+int pm_last_launch_count(pm_handle_t h);
+/* Per-launch durations (ms) recorded since the last call while
+ * PM_OPT_KERNEL_TIMES is on; mode 0 = Stage-1 reduce, 1 = Stage-3 solve,
+ * 2 = root; level 0 = the caller's system.  Synchronises; returns the count. */
+int pm_kernel_times(pm_handle_t h, int32_t* modes, int32_t* levels, float* ms, int32_t max);
+int pm_last_plan(pm_handle_t h, int64_t* rows_per_level, int32_t max_levels);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PM_TRIDIAG_H */

@@ -1,0 +1,760 @@
+// pm_capi.cu -- host orchestration behind the C ABI of include/pm_tridiag.h.
+//
+// Level plan.  Level 0 is the caller's system (m = the sub-system size).
+// Every REDUCE launch turns each CTA tile of level L into two rows of level
+// L+1, so level sizes shrink by T/2 (640x for m = 10); the level whose tiles
+// number one is solved by a single ROOT launch.  Upper levels use m = 8
+// (m = 2 on ranks of a row-sharded solve that are not the last, see
+// pm_dist_*).  A solve is therefore
+//     REDUCE(0) .. REDUCE(top-1), ROOT(top), SOLVE(top-1) .. SOLVE(0)
+// e.g. N = 8e7, m = 10: 8e7 -> 125000 -> 246 rows, five launches.
+//
+// Streams.  pm_solve_host_f64 splits the
+// level-0 tiles into num_streams chunks: per chunk H2D(a,b,c,d) -> REDUCE(0)
+// on its own stream; the upper levels on the main stream after a join;
+// then per chunk SOLVE(0) -> D2H(x).  The reduced system never leaves the
+// device, so the paper's T1^D2H and T3^H2D are zero here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pm_kernels.h"
+#include "pm_tridiag.h"
+#include "streamtune/predictor.hpp"
+
+namespace {
+
+using pm::TileArgs;
+
+struct Level {
+  int64_t n = 0;
+  int m = 10;
+  int P = 128;
+  int64_t T = 0;
+  int64_t ntiles = 0;
+  const double* a = nullptr;
+  const double* b = nullptr;
+  const double* c = nullptr;
+  const double* d = nullptr;
+  double* x = nullptr;
+  bool bulk = true;
+  int pad_mode = 1;
+  int stages = 2;
+};
+
+constexpr size_t kSmemLimit = 226 * 1024;
+
+int choose_P(int m) {
+  if (m <= 16) return 128;
+  if (m <= 32) return 64;
+  return 32;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+struct pm_handle_s {
+  int device = 0;
+  int sm_count = 148;
+  std::string err;
+  // options
+  int stages = 2;
+  int stream_mode = 0;
+  int reverse = 1;
+  int max_ctas = 0;
+  int timings = 0;
+  // device scratch for upper levels (+ dist boundary values)
+  double* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int* dflag = nullptr;
+  // device staging for the host path: a, b, c, d, x
+  double* hbuf = nullptr;
+  size_t hbuf_bytes = 0;
+  std::vector<cudaStream_t> pool;
+  cudaStream_t main = nullptr;
+  cudaStream_t last_stream = nullptr;
+  streamtune::ModelBundle bundle = streamtune::ModelBundle::paper();
+  pm_stage_timings last_t{};
+  double last_total_ms = 0.0;
+  int last_streams = 0;
+  int launches = 0;
+  std::vector<Level> levels;
+  // per-launch CUDA-event timing (PM_OPT_KERNEL_TIMES)
+  int ktimes = 0;
+  std::vector<cudaEvent_t> kev;
+  struct KRec { int mode, level; size_t ev; };
+  std::vector<KRec> krec;
+};
+
+namespace {
+
+int fail(pm_handle_t h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+int cuda_fail(pm_handle_t h, cudaError_t e, const char* what) {
+  return fail(h, PM_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PM_CUDA(h, call)                                     \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return cuda_fail((h), e_, #call); \
+  } while (0)
+
+int ensure_scratch(pm_handle_t h, size_t bytes) {
+  if (bytes <= h->scratch_bytes) return PM_OK;
+  if (h->scratch) {
+    PM_CUDA(h, cudaDeviceSynchronize());
+    PM_CUDA(h, cudaFree(h->scratch));
+    h->scratch = nullptr;
+    h->scratch_bytes = 0;
+  }
+  const size_t want = std::max(bytes, (size_t)1 << 20);
+  PM_CUDA(h, cudaMalloc(&h->scratch, want));
+  h->scratch_bytes = want;
+  return PM_OK;
+}
+
+int pick_stages(int want, int P, int m) {
+  int S = std::max(1, std::min(want, 4));
+  while (S > 1 && pm::tile_smem_bytes(pm::kModeSolve, P, m, S) > kSmemLimit) --S;
+  return S;
+}
+
+// Builds h->levels for a level-0 system; allocates scratch for levels >= 1.
+// ragged0: the caller's last tile must not be padded (row-sharded ranks that
+// are not the last one); then m must divide n and upper levels use m = 2.
+int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b, const double* c,
+               const double* d, double* x, bool ragged0, size_t extra_doubles) {
+  std::vector<Level> lv;
+  Level L0;
+  L0.n = n;
+  L0.m = m;
+  L0.P = choose_P(m);
+  L0.T = (int64_t)L0.P * m;
+  L0.ntiles = (n + L0.T - 1) / L0.T;
+  L0.a = a; L0.b = b; L0.c = c; L0.d = d; L0.x = x;
+  L0.pad_mode = ragged0 ? 0 : 1;
+  L0.stages = pick_stages(h->stages, L0.P, m);
+  if (pm::tile_smem_bytes(pm::kModeSolve, L0.P, m, 1) > kSmemLimit)
+    return fail(h, PM_ERR_VALIDATION, "sub-system size m too large for shared memory");
+  L0.bulk = aligned16(a) && aligned16(b) && aligned16(c) && aligned16(d) && aligned16(x);
+  lv.push_back(L0);
+  while (lv.back().ntiles > 1) {
+    const Level& prev = lv.back();
+    Level U;
+    U.n = 2 * prev.ntiles;
+    U.m = ragged0 ? 2 : 8;
+    U.P = 128;
+    U.T = (int64_t)U.P * U.m;
+    U.ntiles = (U.n + U.T - 1) / U.T;
+    U.pad_mode = ragged0 ? 0 : 1;
+    U.stages = pick_stages(h->stages, U.P, U.m);
+    lv.push_back(U);
+  }
+  // scratch: levels >= 1 hold a, b, c, d, x (n_L each); 256-byte aligned
+  size_t total = extra_doubles;
+  std::vector<size_t> off(lv.size(), 0);
+  for (size_t k = 1; k < lv.size(); ++k) {
+    off[k] = total;
+    total += 5 * (size_t)((lv[k].n + 31) / 32 * 32);
+  }
+  int st = ensure_scratch(h, total * sizeof(double));
+  if (st) return st;
+  for (size_t k = 1; k < lv.size(); ++k) {
+    const size_t stride = (size_t)((lv[k].n + 31) / 32 * 32);
+    double* base = h->scratch + off[k];
+    lv[k].a = base;
+    lv[k].b = base + stride;
+    lv[k].c = base + 2 * stride;
+    lv[k].d = base + 3 * stride;
+    lv[k].x = base + 4 * stride;
+    lv[k].bulk = true;
+  }
+  h->levels = std::move(lv);
+  return PM_OK;
+}
+
+TileArgs args_for(pm_handle_t h, const Level& L, int64_t t0, int64_t t1) {
+  TileArgs A;
+  A.a = L.a; A.b = L.b; A.c = L.c; A.d = L.d; A.x = L.x;
+  A.n = L.n;
+  A.tile_begin = t0;
+  A.tile_end = t1;
+  A.m = L.m;
+  A.stages = L.stages;
+  A.max_ctas = h->max_ctas;
+  A.flag = h->dflag;
+  A.pad_mode = L.pad_mode;
+  return A;
+}
+
+cudaEvent_t next_kevent(pm_handle_t h) {
+  const size_t k = h->krec.size() * 2 + 2;
+  while (h->kev.size() < k) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    h->kev.push_back(e);
+  }
+  return h->kev[k - 2];
+}
+
+int launch(pm_handle_t h, int mode, const TileArgs& A, const Level& L, cudaStream_t st) {
+  int grid = 0;
+  const int level = (int)(&L - h->levels.data());
+  const bool timed = h->ktimes && next_kevent(h) != nullptr;
+  const size_t ev = h->krec.size() * 2;
+  if (timed) cudaEventRecord(h->kev[ev], st);
+  cudaError_t e = pm::launch_tile_kernel(mode, A, L.P, L.bulk, h->sm_count, st, &grid);
+  if (e != cudaSuccess) return cuda_fail(h, e, "tile kernel launch");
+  if (timed) {
+    cudaEventRecord(h->kev[ev + 1], st);
+    h->krec.push_back({mode, level, ev});
+  }
+  if (grid > 0) ++h->launches;
+  return PM_OK;
+}
+
+// REDUCE of level k over tiles [t0, t1): writes rows into level k+1 (or `out4`).
+int enq_reduce(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, bool zf, bool zl,
+               int64_t sys_len, double* const* out4) {
+  const Level& L = h->levels[k];
+  TileArgs A = args_for(h, L, t0, t1);
+  if (out4) {
+    A.ra = out4[0]; A.rb = out4[1]; A.rc = out4[2]; A.rd = out4[3];
+  } else {
+    const Level& U = h->levels[k + 1];
+    A.ra = const_cast<double*>(U.a); A.rb = const_cast<double*>(U.b);
+    A.rc = const_cast<double*>(U.c); A.rd = const_cast<double*>(U.d);
+  }
+  A.zero_first = zf;
+  A.zero_last = zl;
+  A.sys_len = (k == 0) ? sys_len : 0;
+  return launch(h, pm::kModeReduce, A, L, st);
+}
+
+int enq_solve(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, bool zf, bool zl,
+              int64_t sys_len, const double* xb) {
+  const Level& L = h->levels[k];
+  TileArgs A = args_for(h, L, t0, t1);
+  A.xb = xb ? xb : h->levels[k + 1].x;
+  A.zero_first = zf;
+  A.zero_last = zl;
+  A.sys_len = (k == 0) ? sys_len : 0;
+  A.reverse = h->reverse;
+  return launch(h, pm::kModeSolve, A, L, st);
+}
+
+int enq_root(pm_handle_t h, size_t k, cudaStream_t st, int64_t sys_len) {
+  const Level& L = h->levels[k];
+  TileArgs A = args_for(h, L, 0, 1);
+  A.sys_len = (k == 0) ? sys_len : 0;
+  return launch(h, pm::kModeRoot, A, L, st);
+}
+
+// Upper levels (1..top) on one stream: REDUCE 1..top-1, ROOT top, SOLVE top-1..1.
+int enq_upper(pm_handle_t h, cudaStream_t st) {
+  const size_t top = h->levels.size() - 1;
+  int r;
+  for (size_t k = 1; k < top; ++k)
+    if ((r = enq_reduce(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
+  if (top >= 1 && (r = enq_root(h, top, st, 0))) return r;
+  for (size_t k = top; k-- > 1;)
+    if ((r = enq_solve(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
+  return PM_OK;
+}
+
+// Whole solve of the planned system on one stream.
+int enq_full(pm_handle_t h, cudaStream_t st, int64_t sys_len) {
+  int r;
+  if (h->levels.size() == 1) return enq_root(h, 0, st, sys_len);
+  if ((r = enq_reduce(h, 0, 0, h->levels[0].ntiles, st, true, true, sys_len, nullptr))) return r;
+  if ((r = enq_upper(h, st))) return r;
+  return enq_solve(h, 0, 0, h->levels[0].ntiles, st, true, true, sys_len, nullptr);
+}
+
+int validate_common(pm_handle_t h, const void* a, const void* b, const void* c, const void* d,
+                    const void* x, int64_t n, int32_t m) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (!a || !b || !c || !d || !x) return fail(h, PM_ERR_VALIDATION, "null array pointer");
+  if (n < 1) return fail(h, PM_ERR_VALIDATION, "SLAE size must be at least 1");
+  if (m < 2 || m > PM_MAX_M)
+    return fail(h, PM_ERR_VALIDATION,
+                "sub-system size m must lie in [2, " + std::to_string(PM_MAX_M) + "]");
+  return PM_OK;
+}
+
+streamtune::ModelBundle from_c(const pm_model_bundle& c) {
+  streamtune::ModelBundle b;
+  b.sum_a = c.sum_a; b.sum_b = c.sum_b;
+  b.small_a = c.small_a; b.small_b = c.small_b; b.small_c = c.small_c;
+  b.big_a = c.big_a; b.big_b = c.big_b; b.big_c = c.big_c;
+  b.size_threshold = c.size_threshold;
+  b.candidates.clear();
+  for (int k = 0; k < c.num_candidates && k < 5; ++k)
+    b.candidates.push_back(streamtune::StreamCount(c.candidates[k]));
+  return b;
+}
+
+void to_c(const streamtune::ModelBundle& b, pm_model_bundle* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->sum_a = b.sum_a; c->sum_b = b.sum_b;
+  c->small_a = b.small_a; c->small_b = b.small_b; c->small_c = b.small_c;
+  c->big_a = b.big_a; c->big_b = b.big_b; c->big_c = b.big_c;
+  c->size_threshold = b.size_threshold;
+  c->num_candidates = (int32_t)std::min<size_t>(b.candidates.size(), 5);
+  for (int k = 0; k < c->num_candidates; ++k) c->candidates[k] = b.candidates[k].value();
+}
+
+int read_flag(pm_handle_t h, cudaStream_t st) {
+  int flag = 0;
+  PM_CUDA(h, cudaMemcpyAsync(&flag, h->dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PM_CUDA(h, cudaStreamSynchronize(st));
+  if (flag) {
+    PM_CUDA(h, cudaMemsetAsync(h->dflag, 0, sizeof(int), st));
+    PM_CUDA(h, cudaStreamSynchronize(st));
+    return fail(h, PM_ERR_COMPUTATION, "zero or non-finite pivot (system not solvable without pivoting)");
+  }
+  return PM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pm_get_version(void) { return 100; }
+
+int pm_create(pm_handle_t* out, int device) {
+  if (!out) return PM_ERR_VALIDATION;
+  *out = nullptr;
+  pm_handle_t h = new pm_handle_s();
+  h->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaMalloc(&h->dflag, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(h->dflag, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->main, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete h;
+    return PM_ERR_RUNTIME;
+  }
+  *out = h;
+  return PM_OK;
+}
+
+int pm_destroy(pm_handle_t h) {
+  if (!h) return PM_OK;
+  cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (cudaStream_t s : h->pool) cudaStreamDestroy(s);
+  for (cudaEvent_t e : h->kev) cudaEventDestroy(e);
+  if (h->main) cudaStreamDestroy(h->main);
+  if (h->scratch) cudaFree(h->scratch);
+  if (h->hbuf) cudaFree(h->hbuf);
+  if (h->dflag) cudaFree(h->dflag);
+  delete h;
+  return PM_OK;
+}
+
+const char* pm_last_error(pm_handle_t h) { return h ? h->err.c_str() : "null handle"; }
+
+int pm_set_option(pm_handle_t h, int option, int64_t value) {
+  if (!h) return PM_ERR_VALIDATION;
+  switch (option) {
+    case PM_OPT_STAGES:
+      if (value < 1 || value > 4) return fail(h, PM_ERR_VALIDATION, "stages must lie in [1, 4]");
+      h->stages = (int)value;
+      return PM_OK;
+    case PM_OPT_STREAM_MODE:
+      if (value != 0 && value != 1) return fail(h, PM_ERR_VALIDATION, "stream mode is 0 or 1");
+      h->stream_mode = (int)value;
+      return PM_OK;
+    case PM_OPT_REVERSE_SOLVE:
+      h->reverse = value ? 1 : 0;
+      return PM_OK;
+    case PM_OPT_MAX_CTAS:
+      if (value < 0) return fail(h, PM_ERR_VALIDATION, "max_ctas must be >= 0");
+      h->max_ctas = (int)value;
+      return PM_OK;
+    case PM_OPT_TIMINGS:
+      h->timings = value ? 1 : 0;
+      return PM_OK;
+    case PM_OPT_KERNEL_TIMES:
+      h->ktimes = value ? 1 : 0;
+      h->krec.clear();
+      return PM_OK;
+    default:
+      return fail(h, PM_ERR_VALIDATION, "unknown option");
+  }
+}
+
+int pm_solve_device_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                        const double* d, double* x, int64_t n, int32_t m, void* stream) {
+  int r = validate_common(h, a, b, c, d, x, n, m);
+  if (r) return r;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  if ((r = build_plan(h, n, m, a, b, c, d, x, false, 0))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  return enq_full(h, st, 0);
+}
+
+int pm_solve_batch_device_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                              const double* d, double* x, int64_t n_per_system, int64_t batch,
+                              int32_t m, void* stream) {
+  if (batch < 1) return fail(h, PM_ERR_VALIDATION, "batch must be at least 1");
+  if (n_per_system < 1) return fail(h, PM_ERR_VALIDATION, "SLAE size must be at least 1");
+  if (n_per_system > INT64_MAX / batch) return fail(h, PM_ERR_VALIDATION, "batch too large");
+  const int64_t n = n_per_system * batch;
+  int r = validate_common(h, a, b, c, d, x, n, m);
+  if (r) return r;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  if ((r = build_plan(h, n, m, a, b, c, d, x, false, 0))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  return enq_full(h, st, batch > 1 ? n_per_system : 0);
+}
+
+int pm_check(pm_handle_t h) {
+  if (!h) return PM_ERR_VALIDATION;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  cudaStream_t st = h->last_stream;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(h, e, "solve");
+  return read_flag(h, h->main);
+}
+
+int pm_solve_host_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                      const double* d, double* x, int64_t n, int32_t m, int32_t num_streams) {
+  int r = validate_common(h, a, b, c, d, x, n, m);
+  if (r) return r;
+  if (num_streams != 0 && !streamtune::StreamCount::is_valid(num_streams))
+    return fail(h, PM_ERR_VALIDATION,
+                streamtune::InvalidStreamCountError(num_streams).what());
+  PM_CUDA(h, cudaSetDevice(h->device));
+  int ns = num_streams;
+  if (ns == 0) {
+    try {
+      ns = streamtune::recommend(h->bundle, (uint64_t)n).chosen.value();
+    } catch (const std::exception& ex) {
+      return fail(h, PM_ERR_VALIDATION, ex.what());
+    }
+  }
+  // device staging: a, b, c, d, x (x separate so the caller may alias d)
+  const size_t stride = (size_t)((n + 31) / 32 * 32);
+  const size_t need = 5 * stride * sizeof(double);
+  if (need > h->hbuf_bytes) {
+    if (h->hbuf) {
+      PM_CUDA(h, cudaDeviceSynchronize());
+      PM_CUDA(h, cudaFree(h->hbuf));
+      h->hbuf = nullptr;
+      h->hbuf_bytes = 0;
+    }
+    PM_CUDA(h, cudaMalloc(&h->hbuf, need));
+    h->hbuf_bytes = need;
+  }
+  double* da = h->hbuf;
+  double* db = da + stride;
+  double* dc = db + stride;
+  double* dd = dc + stride;
+  double* dx = dd + stride;
+  h->launches = 0;
+  if ((r = build_plan(h, n, m, da, db, dc, dd, dx, false, 0))) return r;
+  const Level& L0 = h->levels[0];
+  const bool single_tile = h->levels.size() == 1;
+  int chunks = single_tile ? 1 : (int)std::min<int64_t>(ns, L0.ntiles);
+
+  cudaStream_t main = h->main;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> evs;
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (h->stream_mode == 1)
+      for (cudaStream_t s : streams) cudaStreamDestroy(s);
+  };
+  cudaEvent_t tev[6];
+  for (int k = 0; k < 6; ++k) {
+    cudaError_t e = cudaEventCreate(&tev[k]);
+    if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaEventCreate"); }
+    evs.push_back(tev[k]);
+  }
+  // The stream set: created inside the timed region in stream mode 1 (the
+  // paper's T_overhead includes creating them).
+  cudaEventRecord(tev[0], main);
+  if (ns > 1) {
+    if (h->stream_mode == 1) {
+      for (int k = 0; k < ns; ++k) {
+        cudaStream_t s;
+        cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaStreamCreate"); }
+        streams.push_back(s);
+      }
+    } else {
+      while ((int)h->pool.size() < ns) {
+        cudaStream_t s;
+        cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaStreamCreate"); }
+        h->pool.push_back(s);
+      }
+      streams.assign(h->pool.begin(), h->pool.begin() + ns);
+    }
+  }
+  const bool record = h->timings && ns == 1;
+  auto bytes_of = [](int64_t rows) { return (size_t)rows * sizeof(double); };
+  cudaError_t e = cudaSuccess;
+  auto h2d = [&](int64_t r0, int64_t r1, cudaStream_t s) {
+    const size_t bytes = bytes_of(r1 - r0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(da + r0, a + r0, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db + r0, b + r0, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dc + r0, c + r0, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dd + r0, d + r0, bytes, cudaMemcpyHostToDevice, s);
+  };
+  auto d2h = [&](int64_t r0, int64_t r1, cudaStream_t s) {
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(x + r0, dx + r0, bytes_of(r1 - r0), cudaMemcpyDeviceToHost, s);
+  };
+
+  if (ns == 1 || chunks <= 1) {
+    h2d(0, n, main);
+    if (record) cudaEventRecord(tev[1], main);
+    if (single_tile) {
+      if (e == cudaSuccess && (r = enq_root(h, 0, main, 0))) { cleanup(); return r; }
+      if (record) { cudaEventRecord(tev[2], main); cudaEventRecord(tev[3], main); }
+    } else {
+      if (e == cudaSuccess && (r = enq_reduce(h, 0, 0, L0.ntiles, main, true, true, 0, nullptr))) { cleanup(); return r; }
+      if (record) cudaEventRecord(tev[2], main);
+      if (e == cudaSuccess && (r = enq_upper(h, main))) { cleanup(); return r; }
+      if (record) cudaEventRecord(tev[3], main);
+      if (e == cudaSuccess && (r = enq_solve(h, 0, 0, L0.ntiles, main, true, true, 0, nullptr))) { cleanup(); return r; }
+    }
+    if (record) cudaEventRecord(tev[4], main);
+    d2h(0, n, main);
+  } else {
+    // fork
+    cudaEvent_t fork, join;
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    evs.push_back(fork);
+    evs.push_back(join);
+    std::vector<cudaEvent_t> done(chunks);
+    for (int k = 0; k < chunks; ++k) {
+      cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+      evs.push_back(done[k]);
+    }
+    cudaEventRecord(fork, main);
+    for (int k = 0; k < chunks; ++k) {
+      const int64_t t0 = L0.ntiles * k / chunks, t1 = L0.ntiles * (k + 1) / chunks;
+      const int64_t r0 = t0 * L0.T, r1 = std::min(n, t1 * L0.T);
+      cudaStream_t s = streams[k];
+      cudaStreamWaitEvent(s, fork, 0);
+      h2d(r0, r1, s);
+      if (e == cudaSuccess && (r = enq_reduce(h, 0, t0, t1, s, true, true, 0, nullptr))) { cleanup(); return r; }
+      cudaEventRecord(done[k], s);
+    }
+    for (int k = 0; k < chunks; ++k) cudaStreamWaitEvent(main, done[k], 0);
+    if (e == cudaSuccess && (r = enq_upper(h, main))) { cleanup(); return r; }
+    cudaEventRecord(join, main);
+    for (int k = 0; k < chunks; ++k) {
+      const int64_t t0 = L0.ntiles * k / chunks, t1 = L0.ntiles * (k + 1) / chunks;
+      const int64_t r0 = t0 * L0.T, r1 = std::min(n, t1 * L0.T);
+      cudaStream_t s = streams[k];
+      cudaStreamWaitEvent(s, join, 0);
+      if (e == cudaSuccess && (r = enq_solve(h, 0, t0, t1, s, true, true, 0, nullptr))) { cleanup(); return r; }
+      d2h(r0, r1, s);
+      cudaEventRecord(done[k], s);
+    }
+    for (int k = 0; k < chunks; ++k) cudaStreamWaitEvent(main, done[k], 0);
+  }
+  if (h->stream_mode == 1) {
+    for (cudaStream_t s : streams) cudaStreamDestroy(s);
+    streams.clear();
+  }
+  cudaEventRecord(tev[5], main);
+  if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaMemcpyAsync"); }
+  cudaError_t se = cudaEventSynchronize(tev[5]);
+  if (se != cudaSuccess) { cleanup(); return cuda_fail(h, se, "solve"); }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, tev[0], tev[5]);
+  h->last_total_ms = ms;
+  h->last_streams = ns;
+  std::memset(&h->last_t, 0, sizeof(h->last_t));
+  h->last_t.slae_size = (uint64_t)n;
+  if (record) {
+    float t[5];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], tev[k], tev[k + 1]);
+    h->last_t.t1_h2d = t[0];
+    h->last_t.t1_comp = t[1];
+    h->last_t.t2_comp = t[2];
+    h->last_t.t3_comp = t[3];
+    h->last_t.t3_d2h = t[4];
+  }
+  cleanup();
+  h->last_stream = main;
+  return read_flag(h, main);
+}
+
+int pm_last_stage_timings(pm_handle_t h, pm_stage_timings* out, double* total_ms,
+                          int32_t* streams_used) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (out) *out = h->last_t;
+  if (total_ms) *total_ms = h->last_total_ms;
+  if (streams_used) *streams_used = h->last_streams;
+  return PM_OK;
+}
+
+int pm_host_register(void* ptr, uint64_t bytes) {
+  if (!ptr || bytes == 0) return PM_ERR_VALIDATION;
+  return cudaHostRegister(ptr, bytes, cudaHostRegisterDefault) == cudaSuccess ? PM_OK : PM_ERR_RUNTIME;
+}
+int pm_host_unregister(void* ptr) {
+  if (!ptr) return PM_ERR_VALIDATION;
+  return cudaHostUnregister(ptr) == cudaSuccess ? PM_OK : PM_ERR_RUNTIME;
+}
+
+int pm_set_model_bundle(pm_handle_t h, const pm_model_bundle* bundle) {
+  if (!h || !bundle) return PM_ERR_VALIDATION;
+  try {
+    streamtune::ModelBundle b = from_c(*bundle);
+    b.validate();
+    h->bundle = b;
+  } catch (const std::exception& ex) {
+    return fail(h, PM_ERR_VALIDATION, ex.what());
+  }
+  return PM_OK;
+}
+
+int pm_get_model_bundle(pm_handle_t h, pm_model_bundle* out) {
+  if (!h || !out) return PM_ERR_VALIDATION;
+  to_c(h->bundle, out);
+  return PM_OK;
+}
+
+int pm_paper_bundle(pm_model_bundle* out) {
+  if (!out) return PM_ERR_VALIDATION;
+  to_c(streamtune::ModelBundle::paper(), out);
+  return PM_OK;
+}
+
+int pm_recommend_streams(int64_t n, const pm_model_bundle* bundle) {
+  if (n < 1) return -1;
+  try {
+    streamtune::ModelBundle b = bundle ? from_c(*bundle) : streamtune::ModelBundle::paper();
+    b.validate();
+    return streamtune::recommend(b, (uint64_t)n).chosen.value();
+  } catch (...) {
+    return -1;
+  }
+}
+
+int pm_generate_f64(pm_handle_t h, double* a, double* b, double* c, double* d, int64_t n,
+                    uint64_t seed, void* stream) {
+  return pm_generate_range_f64(h, a, b, c, d, n, 0, n, seed, stream);
+}
+
+int pm_generate_range_f64(pm_handle_t h, double* a, double* b, double* c, double* d,
+                          int64_t n_total, int64_t row0, int64_t count, uint64_t seed,
+                          void* stream) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (n_total < 1 || count < 1 || row0 < 0 || row0 + count > n_total)
+    return fail(h, PM_ERR_VALIDATION, "row range outside [0, n_total)");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PM_CUDA(h, pm::launch_generate(a, b, c, d, n_total, row0, count, seed, h->sm_count, st));
+  h->last_stream = st;
+  return PM_OK;
+}
+
+int pm_dist_reduce_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                       const double* d, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                       double* iface, void* stream) {
+  // x is not used by the reduce; pass d so the plan's alignment test sees a real pointer
+  int r = validate_common(h, a, b, c, d, d, n_local, m);
+  if (r) return r;
+  if (!iface) return fail(h, PM_ERR_VALIDATION, "null iface pointer");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  const bool last = rank == world - 1;
+  if (!last && n_local % m != 0)
+    return fail(h, PM_ERR_VALIDATION, "n_local must be a multiple of m on every rank but the last");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  // same plan (and the same 32-double prefix) as pm_dist_solve_f64
+  if ((r = build_plan(h, n_local, m, a, b, c, d, const_cast<double*>(d), !last, 32))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  const bool zf = rank == 0, zl = last;
+  const size_t top = h->levels.size() - 1;
+  for (size_t k = 0; k < top; ++k)
+    if ((r = enq_reduce(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
+  double* out4[4] = {iface, iface + 2, iface + 4, iface + 6};
+  return enq_reduce(h, top, 0, 1, st, zf, zl, 0, out4);
+}
+
+int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                      const double* d, double* x, int64_t n_local, int32_t m, int32_t rank,
+                      int32_t world, const double* iface_all, void* stream) {
+  int r = validate_common(h, a, b, c, d, x, n_local, m);
+  if (r) return r;
+  if (!iface_all) return fail(h, PM_ERR_VALIDATION, "null iface_all pointer");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  const bool last = rank == world - 1;
+  if (!last && n_local % m != 0)
+    return fail(h, PM_ERR_VALIDATION, "n_local must be a multiple of m on every rank but the last");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  // two extra doubles in front of the level scratch hold this rank's (xf, xl)
+  if ((r = build_plan(h, n_local, m, a, b, c, d, x, !last, 32))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  double* xb = h->scratch;  // extra_doubles region
+  PM_CUDA(h, pm::launch_dist_chain(iface_all, world, rank, xb, h->dflag, st));
+  ++h->launches;
+  const bool zf = rank == 0, zl = last;
+  const size_t top = h->levels.size() - 1;
+  if ((r = enq_solve(h, top, 0, 1, st, zf, zl, 0, xb))) return r;
+  for (size_t k = top; k-- > 0;)
+    if ((r = enq_solve(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
+  return PM_OK;
+}
+
+int pm_last_launch_count(pm_handle_t h) { return h ? h->launches : -1; }
+
+int pm_kernel_times(pm_handle_t h, int32_t* modes, int32_t* levels, float* ms, int32_t max) {
+  if (!h) return -1;
+  int k = 0;
+  for (const auto& r : h->krec) {
+    if (k >= max) break;
+    float t = 0.f;
+    if (cudaEventSynchronize(h->kev[r.ev + 1]) != cudaSuccess ||
+        cudaEventElapsedTime(&t, h->kev[r.ev], h->kev[r.ev + 1]) != cudaSuccess)
+      return fail(h, -1, "event timing failed"), -1;
+    if (modes) modes[k] = r.mode;
+    if (levels) levels[k] = r.level;
+    if (ms) ms[k] = t;
+    ++k;
+  }
+  h->krec.clear();
+  return k;
+}
+
+int pm_last_plan(pm_handle_t h, int64_t* rows_per_level, int32_t max_levels) {
+  if (!h) return -1;
+  const int nl = (int)h->levels.size();
+  for (int k = 0; k < nl && k < max_levels; ++k)
+    if (rows_per_level) rows_per_level[k] = h->levels[k].n;
+  return nl;
+}
+
+}  // extern "C"

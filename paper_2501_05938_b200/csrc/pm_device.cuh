@@ -1,0 +1,189 @@
+// pm_device.cuh -- device building blocks of the B200 partition-method solver.
+//
+// Algebra (the Austin et al. partition method cited at
+// /root/reference/PAPER.md:26-30, sub-system size m at PAPER.md:52):
+//
+//   A "segment" covers rows f..l (l > f) and is represented by its two
+//   boundary equations in the unknowns just outside / at its ends:
+//     F: Fa*x[f-1] + Fb*x[f] + Fc*x[l]   = Fd
+//     L: La*x[f]   + Lb*x[l] + Lc*x[l+1] = Ld
+//   Stage 1 turns every m-row block into a segment by eliminating its
+//   interior (block_reduce).  Stage 2 (the reduced interface system) is
+//   solved by combining adjacent segments pairwise -- a tree of
+//   "eliminate the two unknowns at the junction" steps (combine) inside a
+//   warp (shuffles), across the warps of a CTA (shared memory), and across
+//   CTA tiles by the same kernels one level up.  The downsweep recovers the
+//   junction unknowns from the stored Node coefficients, and Stage 3
+//   (block_interior) back-substitutes each block's interior from its two
+//   boundary values.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pm {
+
+struct Row {
+  double a, b, c, d;
+};
+struct Seg {
+  Row F, L;
+};
+// Junction solve of a combine:  x[l1] = p0 + p1*x[f1] + p2*x[l2]
+//                               x[f2] = q0 + q1*x[f1] + q2*x[l2]
+struct Node {
+  double p0, p1, p2, q0, q1, q2;
+};
+
+__device__ __forceinline__ double drcp(double x) { return __drcp_rn(x); }
+
+// Merge segment A = [f1..l1] with its right neighbour B = [f2..l2], f2 = l1+1,
+// eliminating x[l1] and x[f2].
+__device__ __forceinline__ void combine(const Seg& A, const Seg& B, Seg& out, Node& nd,
+                                        bool& bad) {
+  const double det = fma(A.L.b, B.F.b, -A.L.c * B.F.a);
+  bad |= (det == 0.0);
+  const double inv = drcp(det);
+  nd.p0 = fma(B.F.b, A.L.d, -A.L.c * B.F.d) * inv;
+  nd.p1 = -(B.F.b * A.L.a) * inv;
+  nd.p2 = (A.L.c * B.F.c) * inv;
+  nd.q0 = fma(A.L.b, B.F.d, -B.F.a * A.L.d) * inv;
+  nd.q1 = (B.F.a * A.L.a) * inv;
+  nd.q2 = -(A.L.b * B.F.c) * inv;
+  Seg o;
+  o.F.a = A.F.a;
+  o.F.b = fma(A.F.c, nd.p1, A.F.b);
+  o.F.c = A.F.c * nd.p2;
+  o.F.d = fma(-A.F.c, nd.p0, A.F.d);
+  o.L.a = B.L.a * nd.q1;
+  o.L.b = fma(B.L.a, nd.q2, B.L.b);
+  o.L.c = B.L.c;
+  o.L.d = fma(-B.L.a, nd.q0, B.L.d);
+  out = o;
+}
+
+__device__ __forceinline__ Seg shfl_down_seg(const Seg& s, int delta) {
+  Seg o;
+  o.F.a = __shfl_down_sync(0xffffffffu, s.F.a, delta);
+  o.F.b = __shfl_down_sync(0xffffffffu, s.F.b, delta);
+  o.F.c = __shfl_down_sync(0xffffffffu, s.F.c, delta);
+  o.F.d = __shfl_down_sync(0xffffffffu, s.F.d, delta);
+  o.L.a = __shfl_down_sync(0xffffffffu, s.L.a, delta);
+  o.L.b = __shfl_down_sync(0xffffffffu, s.L.b, delta);
+  o.L.c = __shfl_down_sync(0xffffffffu, s.L.c, delta);
+  o.L.d = __shfl_down_sync(0xffffffffu, s.L.d, delta);
+  return o;
+}
+
+// ---------------------------------------------------------------------------
+// Per-block (m rows) elimination.  Acc exposes the block's rows (with the
+// boundary fix-ups already applied) as a(j), b(j), c(j), d(j), j = 0..m-1.
+// Interior j = 1..L (L = m-2) is the tridiagonal T with the couplings a(1)
+// (to x[s]) and c(L) (to x[e]) removed; one forward sweep serves the three
+// right-hand sides y (d), g (a(1) e_1), h (c(L) e_L).  The first-interior-
+// row values are accumulated on the fly: y_1 = sum_k P_k y'_k with
+// P_1 = 1, P_{k+1} = -P_k c'_k, so no backward sweep is needed in Stage 1.
+//   F = [a_s, b_s - c_s g_1, -c_s h_1 | d_s - c_s y_1]
+//   L = [-a_e g_L, b_e - a_e h_L, c_e | d_e - a_e y_L]
+// ---------------------------------------------------------------------------
+template <int M, class Acc>
+__device__ __forceinline__ Seg block_reduce(const Acc& r, int m_rt, bool& bad) {
+  const int m = (M > 0) ? M : m_rt;
+  Seg S;
+  if (m == 2) {
+    S.F = Row{r.a(0), r.b(0), r.c(0), r.d(0)};
+    S.L = Row{r.a(1), r.b(1), r.c(1), r.d(1)};
+    return S;
+  }
+  const int L = m - 2;
+  double den = r.b(1);
+  bad |= (den == 0.0);
+  double inv = drcp(den);
+  double cp = (L > 1) ? r.c(1) * inv : 0.0;
+  double yp = r.d(1) * inv;
+  double gp = r.a(1) * inv;
+  double P = 1.0, Y1 = yp, G1 = gp;
+  auto step = [&](int j) {
+    const double aj = r.a(j);
+    den = fma(-aj, cp, r.b(j));
+    bad |= (den == 0.0);
+    inv = drcp(den);
+    P = -P * cp;
+    yp = fma(-aj, yp, r.d(j)) * inv;
+    gp = -aj * gp * inv;
+    cp = (j < L) ? r.c(j) * inv : 0.0;
+    Y1 = fma(P, yp, Y1);
+    G1 = fma(P, gp, G1);
+  };
+  if constexpr (M > 0) {
+#pragma unroll
+    for (int j = 2; j <= M - 2; ++j) step(j);
+  } else {
+    for (int j = 2; j <= L; ++j) step(j);
+  }
+  const double hL = r.c(L) * inv;
+  const double H1 = P * hL;
+  const double as = r.a(0), bs = r.b(0), cs = r.c(0), ds = r.d(0);
+  const double ae = r.a(m - 1), be = r.b(m - 1), ce = r.c(m - 1), de = r.d(m - 1);
+  S.F = Row{as, fma(-cs, G1, bs), -cs * H1, fma(-cs, Y1, ds)};
+  S.L = Row{-ae * gp, fma(-ae, hL, be), ce, fma(-ae, yp, de)};
+  return S;
+}
+
+// Stage 3 for one block: Thomas on the interior with known x[s] = xs and
+// x[e] = xe folded into the right-hand side.  Writes x(j) for j = 0..m-1
+// through r.set_x.  Acc must also provide scratch set_cp/cp, set_dp/dp.
+template <int M, class Acc>
+__device__ __forceinline__ void block_interior(Acc& r, int m_rt, double xs, double xe,
+                                               bool& bad) {
+  const int m = (M > 0) ? M : m_rt;
+  if (m == 2) {
+    r.set_x(0, xs);
+    r.set_x(1, xe);
+    return;
+  }
+  const int L = m - 2;
+  double den = r.b(1);
+  bad |= (den == 0.0);
+  double inv = drcp(den);
+  double rhs = fma(-r.a(1), xs, r.d(1));
+  if (L == 1) rhs = fma(-r.c(1), xe, rhs);
+  double cp = (L > 1) ? r.c(1) * inv : 0.0;
+  double dp = rhs * inv;
+  r.set_cp(1, cp);
+  r.set_dp(1, dp);
+  auto fwd = [&](int j) {
+    const double aj = r.a(j);
+    den = fma(-aj, cp, r.b(j));
+    bad |= (den == 0.0);
+    inv = drcp(den);
+    rhs = r.d(j);
+    if (j == L) rhs = fma(-r.c(j), xe, rhs);
+    cp = (j < L) ? r.c(j) * inv : 0.0;
+    dp = fma(-aj, dp, rhs) * inv;
+    r.set_cp(j, cp);
+    r.set_dp(j, dp);
+  };
+  double xn;
+  auto bwd = [&](int j) {
+    xn = fma(-r.cp(j), xn, r.dp(j));
+    r.set_x(j, xn);
+  };
+  if constexpr (M > 0) {
+#pragma unroll
+    for (int j = 2; j <= M - 2; ++j) fwd(j);
+    xn = dp;  // x_L
+    r.set_x(L, xn);
+#pragma unroll
+    for (int j = M - 3; j >= 1; --j) bwd(j);
+  } else {
+    for (int j = 2; j <= L; ++j) fwd(j);
+    xn = dp;
+    r.set_x(L, xn);
+    for (int j = L - 1; j >= 1; --j) bwd(j);
+  }
+  r.set_x(0, xs);
+  r.set_x(m - 1, xe);
+}
+
+}  // namespace pm

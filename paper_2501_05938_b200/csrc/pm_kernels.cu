@@ -1,0 +1,680 @@
+// pm_kernels.cu -- sm_100a kernels of the partition-method solver.
+//
+// One persistent kernel template, three modes, applied level by level:
+//   REDUCE  (Stage 1, "kernel responsible for Stage 1"):
+//           every CTA tile of T = P*m rows -> per-thread m-block elimination
+//           -> warp/CTA combine tree -> the tile's two interface equations,
+//           written as rows 2t, 2t+1 of the next level's system.
+//   ROOT    the top level (<= one tile): reduce, solve the final 2x2, and
+//           run the downsweep + back-substitution in the same CTA.
+//   SOLVE   (Stage 3, "kernel responsible for Stage 3"): re-read
+//           the tile, recompute the tree, start the downsweep from the
+//           tile's two boundary values (the level above's x), back-
+//           substitute every block interior, store x.
+// The reduced interface system of the paper's Stage 2 (solved
+// on the CPU there) is therefore solved on the GPU by the combine trees and
+// the upper levels (north_star: "warp and block-level recursive
+// partition/PCR solve, with no CPU fallback").
+//
+// Data movement: a,b,c,d tiles arrive in shared memory through 1-D bulk
+// async copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier ring
+// of `stages` buffers; x tiles leave through bulk stores.  Loads for tile
+// k+stages are in flight while tile k is computed.  Grids are persistent:
+// ctas_per_sm * #SMs CTAs striding over the tiles.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "pm_device.cuh"
+#include "pm_kernels.h"
+
+namespace pm {
+
+constexpr int kMaxStages = 4;
+constexpr int kMaxWarps = 8;  // P <= 256
+
+// ---------------------------------------------------------------------------
+// PTX helpers (mbarrier + bulk copies)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Row accessors
+// ---------------------------------------------------------------------------
+// Boundary fix-ups shared by both accessors (rows of one tile):
+//   local row >= valid      -> identity padding row (a=c=d=0, b=1)
+//   global row 0            -> a = 0   (a[0] is ignored by contract)
+//   global row n-1          -> c = 0   (c[n-1] is ignored by contract)
+//   odd tail row not covered by the 16-byte bulk copy -> read from global.
+struct TileCtx {
+  const double* ga;
+  const double* gb;
+  const double* gc;
+  const double* gd;
+  int64_t row0;   // first global row of the tile
+  int64_t n;      // rows of this level
+  int valid;      // rows of the tile inside [0, n)
+  bool odd_tail;  // row valid-1 must be read from global
+  bool zf, zl;    // zero a[0] / c[n-1]
+  int64_t sys_len;
+};
+
+// Does the block starting at tile row lr0 (m rows) need any fix-up?
+__device__ __forceinline__ bool block_needs_fixup(const TileCtx& t, int lr0, int m) {
+  const int64_t g0 = t.row0 + lr0;
+  if (g0 == 0 || g0 + m > t.n - 1) return true;
+  if (t.sys_len) {
+    const int64_t rem = g0 % t.sys_len;
+    return rem == 0 || rem + m > t.sys_len - 1;
+  }
+  return false;
+}
+
+__device__ __forceinline__ void fixup_row(const TileCtx& t, int lr, double& a, double& b,
+                                          double& c, double& d) {
+  if (lr >= t.valid) {
+    a = 0.0;
+    b = 1.0;
+    c = 0.0;
+    d = 0.0;
+    return;
+  }
+  const int64_t g = t.row0 + lr;
+  if (t.odd_tail && lr == t.valid - 1) {
+    a = __ldg(t.ga + g);
+    b = __ldg(t.gb + g);
+    c = __ldg(t.gc + g);
+    d = __ldg(t.gd + g);
+  }
+  if (t.zf && g == 0) a = 0.0;
+  if (t.zl && g == t.n - 1) c = 0.0;
+  if (t.sys_len) {
+    const int64_t rem = g % t.sys_len;
+    if (rem == 0) a = 0.0;
+    if (rem == t.sys_len - 1) c = 0.0;
+  }
+}
+
+// Compile-time m: the block's rows live in registers.
+template <int M>
+struct RegAcc {
+  double A[M], B[M], C[M], D[M];  // C/D are reused for c'/d' in Stage 3, B for x
+  __device__ __forceinline__ double a(int j) const { return A[j]; }
+  __device__ __forceinline__ double b(int j) const { return B[j]; }
+  __device__ __forceinline__ double c(int j) const { return C[j]; }
+  __device__ __forceinline__ double d(int j) const { return D[j]; }
+  __device__ __forceinline__ void set_cp(int j, double v) { C[j] = v; }
+  __device__ __forceinline__ double cp(int j) const { return C[j]; }
+  __device__ __forceinline__ void set_dp(int j, double v) { D[j] = v; }
+  __device__ __forceinline__ double dp(int j) const { return D[j]; }
+  __device__ __forceinline__ void set_x(int j, double v) { B[j] = v; }
+  __device__ __forceinline__ double x(int j) const { return B[j]; }
+
+  __device__ __forceinline__ void load(const double* sa, const double* sb, const double* sc,
+                                       const double* sd, int r0, const TileCtx& t) {
+    if constexpr ((M % 2) == 0) {
+      const double2* pa = reinterpret_cast<const double2*>(sa + r0);
+      const double2* pb = reinterpret_cast<const double2*>(sb + r0);
+      const double2* pc = reinterpret_cast<const double2*>(sc + r0);
+      const double2* pd = reinterpret_cast<const double2*>(sd + r0);
+#pragma unroll
+      for (int j = 0; j < M / 2; ++j) {
+        double2 va = pa[j], vb = pb[j], vc = pc[j], vd = pd[j];
+        A[2 * j] = va.x; A[2 * j + 1] = va.y;
+        B[2 * j] = vb.x; B[2 * j + 1] = vb.y;
+        C[2 * j] = vc.x; C[2 * j + 1] = vc.y;
+        D[2 * j] = vd.x; D[2 * j + 1] = vd.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        A[j] = sa[r0 + j]; B[j] = sb[r0 + j]; C[j] = sc[r0 + j]; D[j] = sd[r0 + j];
+      }
+    }
+    // rare: only blocks touching row 0, row n-1, a system boundary or the tail
+    if (block_needs_fixup(t, r0, M)) {
+#pragma unroll
+      for (int j = 0; j < M; ++j) fixup_row(t, r0 + j, A[j], B[j], C[j], D[j]);
+    }
+  }
+  __device__ __forceinline__ void store_x(double* xbuf, int r0) const {
+    if constexpr ((M % 2) == 0) {
+      double2* px = reinterpret_cast<double2*>(xbuf + r0);
+#pragma unroll
+      for (int j = 0; j < M / 2; ++j) px[j] = make_double2(B[2 * j], B[2 * j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) xbuf[r0 + j] = B[j];
+    }
+  }
+};
+
+// Runtime m: rows stay in the shared-memory stage; c'/d' overwrite c/d in
+// place and x goes to the tile's x buffer.
+struct SmemAcc {
+  double* sa;
+  double* sb;
+  double* sc;
+  double* sd;
+  double* sx;
+  __device__ __forceinline__ double a(int j) const { return sa[j]; }
+  __device__ __forceinline__ double b(int j) const { return sb[j]; }
+  __device__ __forceinline__ double c(int j) const { return sc[j]; }
+  __device__ __forceinline__ double d(int j) const { return sd[j]; }
+  __device__ __forceinline__ void set_cp(int j, double v) { sc[j] = v; }
+  __device__ __forceinline__ double cp(int j) const { return sc[j]; }
+  __device__ __forceinline__ void set_dp(int j, double v) { sd[j] = v; }
+  __device__ __forceinline__ double dp(int j) const { return sd[j]; }
+  __device__ __forceinline__ void set_x(int j, double v) { sx[j] = v; }
+  __device__ __forceinline__ double x(int j) const { return sx[j]; }
+
+  __device__ __forceinline__ void fixup(int r0, int m, const TileCtx& t) {
+    if (block_needs_fixup(t, r0, m)) {
+      for (int j = 0; j < m; ++j) {
+        double a0 = sa[j], b0 = sb[j], c0 = sc[j], d0 = sd[j];
+        fixup_row(t, r0 + j, a0, b0, c0, d0);
+        sa[j] = a0; sb[j] = b0; sc[j] = c0; sd[j] = d0;
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// CTA combine tree
+// ---------------------------------------------------------------------------
+struct TreeSmem {
+  Seg wseg[kMaxWarps];
+  double2 wx[kMaxWarps];
+  Node cnodes[kMaxWarps];
+};
+
+__device__ __forceinline__ int warp_node_off(int k) { return 32 - (32 >> k); }
+
+// Upsweep.  Leaves: one segment per thread.  Result valid in thread 0.
+// Stores Node coefficients when `wnodes` is non-null.
+// `nblk` = number of non-empty leaf blocks (a prefix); the trailing blocks of
+// a ragged tile are empty segments and combine as the identity.
+__device__ __forceinline__ Seg cta_upsweep(Seg s, TreeSmem& tr, Node* wnodes, int lane, int warp,
+                                           int nwarps, int nblk, bool& bad) {
+  const bool keep = (wnodes != nullptr);
+  const int blk = warp * 32 + lane;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int stride = 1 << k;
+    Seg o = shfl_down_seg(s, stride);
+    if ((lane & (2 * stride - 1)) == 0 && blk + stride < nblk) {
+      Node nd;
+      combine(s, o, s, nd, bad);
+      if (keep) wnodes[warp * 31 + warp_node_off(k) + (lane >> (k + 1))] = nd;
+    }
+  }
+  if (nwarps > 1) {
+    if (lane == 0) tr.wseg[warp] = s;
+    __syncthreads();
+    if (warp == 0) {
+      s = tr.wseg[lane < nwarps ? lane : 0];
+      for (int k = 0; (1 << k) < nwarps; ++k) {
+        const int stride = 1 << k;
+        Seg o = shfl_down_seg(s, stride);
+        if (lane < nwarps && (lane & (2 * stride - 1)) == 0 && (lane + stride) * 32 < nblk) {
+          Node nd;
+          combine(s, o, s, nd, bad);
+          if (keep) tr.cnodes[nwarps - (nwarps >> k) + (lane >> (k + 1))] = nd;
+        }
+      }
+    }
+  }
+  return s;
+}
+
+// One downsweep level inside a warp: lanes that were left operands at
+// stride `stride` split their (xf, xl) with the stored node and hand the
+// right half to lane + stride.
+__device__ __forceinline__ void down_level(const Node* nodes, int stride, int lane, int active,
+                                           bool right_nonempty, double& xf, double& xl) {
+  const bool left = lane < active && (lane & (2 * stride - 1)) == 0 && right_nonempty;
+  double sf = 0.0, sl = 0.0;
+  if (left) {
+    const Node nd = nodes[lane / (2 * stride)];
+    const double xl1 = fma(nd.p2, xl, fma(nd.p1, xf, nd.p0));
+    const double xf2 = fma(nd.q2, xl, fma(nd.q1, xf, nd.q0));
+    sf = xf2;
+    sl = xl;
+    xl = xl1;
+  }
+  const double rf = __shfl_up_sync(0xffffffffu, sf, stride);
+  const double rl = __shfl_up_sync(0xffffffffu, sl, stride);
+  if (lane < active && (lane & (2 * stride - 1)) == stride) {
+    xf = rf;
+    xl = rl;
+  }
+}
+
+// Downsweep.  (xf, xl) of the tile are valid in thread 0 on entry; on exit
+// every thread holds (x_s, x_e) of its own block.
+__device__ __forceinline__ void cta_downsweep(double& xf, double& xl, TreeSmem& tr,
+                                              const Node* wnodes, int lane, int warp, int nwarps,
+                                              int nblk) {
+  if (nwarps > 1) {
+    if (warp == 0) {
+      int levels = 0;
+      while ((1 << levels) < nwarps) ++levels;
+      for (int k = levels - 1; k >= 0; --k)
+        down_level(tr.cnodes + (nwarps - (nwarps >> k)), 1 << k, lane, nwarps,
+                   (lane + (1 << k)) * 32 < nblk, xf, xl);
+      if (lane < nwarps) tr.wx[lane] = make_double2(xf, xl);
+    }
+    __syncthreads();
+    const double2 v = tr.wx[warp];
+    xf = v.x;
+    xl = v.y;
+  }
+  const int blk = warp * 32 + lane;
+#pragma unroll
+  for (int k = 4; k >= 0; --k)
+    down_level(wnodes + warp * 31 + warp_node_off(k), 1 << k, lane, 32, blk + (1 << k) < nblk,
+               xf, xl);
+}
+
+// ---------------------------------------------------------------------------
+// The tile kernel
+// ---------------------------------------------------------------------------
+template <int M, int MODE, bool BULK>
+__global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t bars[kMaxStages];
+  __shared__ TreeSmem tree;
+
+  const int P = blockDim.x;
+  const int m = (M > 0) ? M : args.m;
+  const int T = P * m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = P >> 5;
+  const int S = BULK ? args.stages : 1;
+  const int r0 = tid * m;
+
+  double* stage0 = reinterpret_cast<double*>(smem_raw);
+  double* xbuf = stage0 + (size_t)S * 4 * T;
+  Node* wnodes = reinterpret_cast<Node*>(xbuf + (MODE == kModeReduce ? 0 : T));
+
+  const int64_t ntiles = args.tile_end - args.tile_begin;
+  const int64_t nlocal =
+      (ntiles > blockIdx.x) ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto tile_of = [&](int64_t k) -> int64_t {
+    const int64_t idx = blockIdx.x + k * gridDim.x;
+    return args.reverse ? (args.tile_end - 1 - idx) : (args.tile_begin + idx);
+  };
+  auto stage_ptr = [&](int s, int q) -> double* { return stage0 + ((size_t)s * 4 + q) * T; };
+
+  auto issue = [&](int s, int64_t t) {
+    const int64_t row0 = t * T;
+    const int64_t v = (args.n - row0 < T) ? (args.n - row0) : T;
+    const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(1)) * 8);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&bars[s], 4u * bytes);
+    if (bytes) {
+      bulk_g2s(stage_ptr(s, 0), args.a + row0, bytes, &bars[s]);
+      bulk_g2s(stage_ptr(s, 1), args.b + row0, bytes, &bars[s]);
+      bulk_g2s(stage_ptr(s, 2), args.c + row0, bytes, &bars[s]);
+      bulk_g2s(stage_ptr(s, 3), args.d + row0, bytes, &bars[s]);
+    }
+  };
+
+  if constexpr (BULK) {
+    if (tid == 0) {
+      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int s = 0; s < S && s < nlocal; ++s) issue(s, tile_of(s));
+  }
+
+  bool bad = false;
+  for (int64_t k = 0; k < nlocal; ++k) {
+    const int64_t t = tile_of(k);
+    const int s = BULK ? static_cast<int>(k % S) : 0;
+    TileCtx ctx;
+    ctx.ga = args.a; ctx.gb = args.b; ctx.gc = args.c; ctx.gd = args.d;
+    ctx.row0 = t * T;
+    ctx.n = args.n;
+    ctx.valid = static_cast<int>((args.n - ctx.row0 < T) ? (args.n - ctx.row0) : T);
+    ctx.odd_tail = BULK && (ctx.valid & 1);
+    ctx.zf = args.zero_first != 0;
+    ctx.zl = args.zero_last != 0;
+    ctx.sys_len = args.sys_len;
+    // non-empty leaf blocks of this tile (pad mode: all P)
+    const int nblk = args.pad_mode ? P : (ctx.valid + m - 1) / m;
+    double* sa = stage_ptr(s, 0);
+    double* sb = stage_ptr(s, 1);
+    double* sc = stage_ptr(s, 2);
+    double* sd = stage_ptr(s, 3);
+
+    if constexpr (BULK) {
+      mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
+    } else {
+      __syncthreads();  // previous tile done with the stage and xbuf
+      for (int i = tid; i < T; i += P) {
+        const bool in = i < ctx.valid;
+        const int64_t g = ctx.row0 + i;
+        sa[i] = in ? args.a[g] : 0.0;
+        sb[i] = in ? args.b[g] : 0.0;
+        sc[i] = in ? args.c[g] : 0.0;
+        sd[i] = in ? args.d[g] : 0.0;
+      }
+      __syncthreads();
+    }
+
+    // ---- Stage 1 for this thread's m-block ------------------------------
+    Seg seg;
+    RegAcc<(M > 0 ? M : 1)> regs;
+    SmemAcc sacc{sa + r0, sb + r0, sc + r0, sd + r0, xbuf + r0};
+    if constexpr (M > 0) {
+      regs.load(sa, sb, sc, sd, r0, ctx);
+      if constexpr (BULK) {
+        __syncthreads();  // stage s fully consumed -> refill it
+        if (tid == 0 && k + S < nlocal) issue(s, tile_of(k + S));
+      }
+      seg = block_reduce<M>(regs, m, bad);
+    } else {
+      sacc.fixup(r0, m, ctx);
+      seg = block_reduce<0>(sacc, m, bad);
+      if constexpr (BULK && MODE == kModeReduce) {
+        __syncthreads();
+        if (tid == 0 && k + S < nlocal) issue(s, tile_of(k + S));
+      }
+    }
+
+    // ---- Stage 2: combine tree over the tile's blocks ----------------------
+    Seg top = cta_upsweep(seg, tree, MODE == kModeReduce ? nullptr : wnodes, lane, warp, nwarps,
+                          nblk, bad);
+    if constexpr (MODE == kModeReduce) {
+      if (tid == 0) {
+        args.ra[2 * t] = top.F.a; args.rb[2 * t] = top.F.b;
+        args.rc[2 * t] = top.F.c; args.rd[2 * t] = top.F.d;
+        args.ra[2 * t + 1] = top.L.a; args.rb[2 * t + 1] = top.L.b;
+        args.rc[2 * t + 1] = top.L.c; args.rd[2 * t + 1] = top.L.d;
+      }
+    } else {
+      double xf = 0.0, xl = 0.0;
+      if (tid == 0) {
+        if constexpr (MODE == kModeRoot) {
+          // top.F.a and top.L.c multiply unknowns outside the system (zero).
+          const double det = fma(top.F.b, top.L.b, -top.F.c * top.L.a);
+          bad |= (det == 0.0);
+          const double inv = drcp(det);
+          xf = fma(top.F.d, top.L.b, -top.F.c * top.L.d) * inv;
+          xl = fma(top.F.b, top.L.d, -top.L.a * top.F.d) * inv;
+        } else {
+          xf = args.xb[2 * t];
+          xl = args.xb[2 * t + 1];
+        }
+        if constexpr (BULK) bulk_wait_read0();  // previous x tile left xbuf
+      }
+      __syncthreads();
+      cta_downsweep(xf, xl, tree, wnodes, lane, warp, nwarps, nblk);
+
+      // ---- Stage 3: back-substitute this block's interior -----------------
+      if constexpr (M > 0) {
+        block_interior<M>(regs, m, xf, xl, bad);
+#pragma unroll
+        for (int j = 0; j < M; ++j) bad |= !isfinite(regs.x(j));
+        regs.store_x(xbuf, r0);
+        if (ctx.odd_tail && r0 <= ctx.valid - 1 && ctx.valid - 1 < r0 + M) {
+#pragma unroll
+          for (int j = 0; j < M; ++j)
+            if (r0 + j == ctx.valid - 1) args.x[ctx.row0 + r0 + j] = regs.x(j);
+        }
+      } else {
+        block_interior<0>(sacc, m, xf, xl, bad);
+        for (int j = 0; j < m; ++j) bad |= !isfinite(sacc.x(j));
+        if (ctx.odd_tail && r0 <= ctx.valid - 1 && ctx.valid - 1 < r0 + m)
+          args.x[ctx.row0 + ctx.valid - 1] = sacc.x(ctx.valid - 1 - r0);
+      }
+      if constexpr (BULK) {
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+          const uint32_t bytes = static_cast<uint32_t>((ctx.valid & ~1) * 8);
+          if (bytes) {
+            bulk_s2g(args.x + ctx.row0, xbuf, bytes);
+            bulk_commit();
+          }
+          if constexpr (M == 0) {
+            if (k + S < nlocal) issue(s, tile_of(k + S));
+          }
+        }
+      } else {
+        __syncthreads();
+        for (int i = tid; i < ctx.valid; i += P) args.x[ctx.row0 + i] = xbuf[i];
+      }
+    }
+  }
+  if constexpr (BULK && MODE != kModeReduce) {
+    if (tid == 0) bulk_wait0();
+  }
+  if (bad) atomicOr(args.flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Row-sharded solve: the 2*world-row interface system, solved redundantly by
+// one thread on every rank.  Segment k = rank k's two
+// interface equations; chain-combine 0..world-1 keeping the nodes, solve the
+// final 2x2 (rank 0's F.a and rank world-1's L.c are zero), then walk the
+// chain back down to this rank.
+// ---------------------------------------------------------------------------
+__global__ void dist_chain_kernel(const double* __restrict__ iface, int world, int rank,
+                                  double* __restrict__ xb, int* flag) {
+  extern __shared__ Node chain_nodes[];
+  if (threadIdx.x != 0) return;
+  bool bad = false;
+  // per rank: [Fa, La, Fb, Lb, Fc, Lc, Fd, Ld] (the REDUCE kernel's output
+  // layout for a one-tile level: ra = p, rb = p + 2, rc = p + 4, rd = p + 6)
+  auto seg_of = [&](int k) {
+    const double* p = iface + 8 * k;
+    return Seg{Row{p[0], p[2], p[4], p[6]}, Row{p[1], p[3], p[5], p[7]}};
+  };
+  Seg acc = seg_of(0);
+  for (int k = 1; k < world; ++k) {
+    Node nd;
+    combine(acc, seg_of(k), acc, nd, bad);
+    chain_nodes[k] = nd;
+  }
+  const double det = fma(acc.F.b, acc.L.b, -acc.F.c * acc.L.a);
+  bad |= (det == 0.0);
+  const double inv = drcp(det);
+  const double x0 = fma(acc.F.d, acc.L.b, -acc.F.c * acc.L.d) * inv;  // x_first of rank 0
+  double xl = fma(acc.F.b, acc.L.d, -acc.L.a * acc.F.d) * inv;        // x_last of rank k
+  double xf = x0;
+  for (int k = world - 1; k >= 1 && k >= rank; --k) {
+    const Node nd = chain_nodes[k];
+    const double xl_prev = fma(nd.p2, xl, fma(nd.p1, x0, nd.p0));
+    const double xf_k = fma(nd.q2, xl, fma(nd.q1, x0, nd.q0));
+    if (k == rank) {
+      xf = xf_k;
+      break;
+    }
+    xl = xl_prev;
+  }
+  xb[0] = xf;
+  xb[1] = xl;
+  if (bad || !isfinite(xf) || !isfinite(xl)) atomicOr(flag, 1);
+}
+
+cudaError_t launch_dist_chain(const double* iface_all, int world, int rank, double* xb, int* flag,
+                              cudaStream_t st) {
+  const size_t smem = (size_t)world * sizeof(Node);
+  if (smem > 48 * 1024) return cudaErrorInvalidValue;
+  dist_chain_kernel<<<1, 32, smem, st>>>(iface_all, world, rank, xb, flag);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Counter-based generator (bit-identical to oracle/tridiag_oracle.c)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void generate_kernel(double* a, double* b, double* c, double* d, int64_t n,
+                                int64_t row0, int64_t count, uint64_t ka, uint64_t kb,
+                                uint64_t kc, uint64_t kd, uint64_t ks) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = row0 + k;
+    const uint64_t u = static_cast<uint64_t>(i);
+    const double ua = __dmul_rn((double)(splitmix64(ka + u) >> 11), 0x1.0p-53);
+    const double uc = __dmul_rn((double)(splitmix64(kc + u) >> 11), 0x1.0p-53);
+    const double ub = __dmul_rn((double)(splitmix64(kb + u) >> 11), 0x1.0p-53);
+    const double ud = __dmul_rn((double)(splitmix64(kd + u) >> 11), 0x1.0p-53);
+    const double ai = (i == 0) ? 0.0 : __dadd_rn(__dmul_rn(2.0, ua), -1.0);
+    const double ci = (i == n - 1) ? 0.0 : __dadd_rn(__dmul_rn(2.0, uc), -1.0);
+    const double mag = __dadd_rn(__dadd_rn(__dadd_rn(fabs(ai), fabs(ci)), 1.0), ub);
+    const double bi = (splitmix64(ks + u) >> 63) ? -mag : mag;
+    if (a) a[k] = ai;
+    if (b) b[k] = bi;
+    if (c) c[k] = ci;
+    if (d) d[k] = __dadd_rn(__dmul_rn(2.0, ud), -1.0);
+  }
+}
+
+static uint64_t splitmix64_host(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t key_host(uint64_t seed, uint64_t arr) {
+  return splitmix64_host(seed ^ (0x632BE59BD9B4E019ull * (arr + 1ull)));
+}
+
+cudaError_t launch_generate(double* a, double* b, double* c, double* d, int64_t n,
+                            int64_t row0, int64_t count, uint64_t seed, int sm_count,
+                            cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int threads = 256;
+  int64_t blocks = (count + threads - 1) / threads;
+  const int64_t cap = (int64_t)sm_count * 8;
+  if (blocks > cap) blocks = cap;
+  generate_kernel<<<(unsigned)blocks, threads, 0, st>>>(a, b, c, d, n, row0, count, key_host(seed, 0),
+                                                       key_host(seed, 2), key_host(seed, 1),
+                                                       key_host(seed, 3), key_host(seed, 4));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launch plumbing
+// ---------------------------------------------------------------------------
+size_t tile_smem_bytes(int mode, int P, int m, int stages) {
+  const size_t T = (size_t)P * m;
+  size_t bytes = (size_t)stages * 4 * T * sizeof(double);
+  if (mode != kModeReduce) {
+    bytes += T * sizeof(double);                          // x buffer
+    bytes += (size_t)(P / 32) * 31 * sizeof(Node);        // warp-level nodes
+  }
+  return bytes;
+}
+
+template <int M, int MODE, bool BULK>
+static cudaError_t launch_one(const TileArgs& args, int P, int sm_count, cudaStream_t st,
+                              int* grid_out) {
+  auto kern = tile_kernel<M, MODE, BULK>;
+  const int S = BULK ? args.stages : 1;
+  const size_t smem = tile_smem_bytes(MODE, P, (M > 0 ? M : args.m), S);
+  static thread_local size_t configured = 0;  // per-instantiation attribute cache
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int64_t ntiles = args.tile_end - args.tile_begin;
+  int64_t grid = (int64_t)per_sm * sm_count;
+  if (args.max_ctas > 0 && grid > args.max_ctas) grid = args.max_ctas;
+  if (grid > ntiles) grid = ntiles;
+  if (grid_out) *grid_out = (int)grid;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<(unsigned)grid, P, smem, st>>>(args);
+  return cudaGetLastError();
+}
+
+template <int MODE, bool BULK>
+static cudaError_t dispatch_m(int Mspec, const TileArgs& args, int P, int sm_count,
+                              cudaStream_t st, int* grid_out) {
+  switch (Mspec) {
+    case 2: return launch_one<2, MODE, BULK>(args, P, sm_count, st, grid_out);
+    case 8: return launch_one<8, MODE, BULK>(args, P, sm_count, st, grid_out);
+    case 10: return launch_one<10, MODE, BULK>(args, P, sm_count, st, grid_out);
+    default: return launch_one<0, MODE, BULK>(args, P, sm_count, st, grid_out);
+  }
+}
+
+bool m_is_specialised(int m) { return m == 2 || m == 8 || m == 10; }
+
+cudaError_t launch_tile_kernel(int mode, const TileArgs& args, int P, bool bulk, int sm_count,
+                               cudaStream_t st, int* grid_out) {
+  const int Mspec = m_is_specialised(args.m) ? args.m : 0;
+  if (mode == kModeReduce)
+    return bulk ? dispatch_m<kModeReduce, true>(Mspec, args, P, sm_count, st, grid_out)
+                : dispatch_m<kModeReduce, false>(Mspec, args, P, sm_count, st, grid_out);
+  if (mode == kModeSolve)
+    return bulk ? dispatch_m<kModeSolve, true>(Mspec, args, P, sm_count, st, grid_out)
+                : dispatch_m<kModeSolve, false>(Mspec, args, P, sm_count, st, grid_out);
+  return bulk ? dispatch_m<kModeRoot, true>(Mspec, args, P, sm_count, st, grid_out)
+              : dispatch_m<kModeRoot, false>(Mspec, args, P, sm_count, st, grid_out);
+}
+
+}  // namespace pm

@@ -1,0 +1,58 @@
+"""Row-sharded single system over ranks (BASELINE.json config 5).
+
+One process per GPU.  Rank r owns the contiguous rows [off_r, off_r + n_r).
+The only cross-GPU step is the all-gather of every rank's two interface
+equations (8 doubles = 64 B per rank, NCCL over NVLink):
+
+    pm_dist_reduce_f64   Stage 1 + local upper levels -> iface (8 doubles)
+    all_gather(iface)    -> iface_all (8 * world doubles, rank order)
+    pm_dist_solve_f64    2*world-row interface system (redundant, one thread)
+                         -> local Stage 3 of every level -> x
+
+`split_rows` gives every rank but the last a multiple of m rows (the solver
+requires it there: a non-last rank's final m-block must be complete so its
+last interface row is a real row, not padding).
+"""
+from __future__ import annotations
+
+from .errors import ValidationError
+
+
+def split_rows(n: int, world: int, m: int) -> list[int]:
+    if world < 1 or n < 1:
+        raise ValidationError("need n >= 1 and world >= 1")
+    if world == 1:
+        return [n]
+    q = max(m, (n // world) // m * m)
+    last = n - q * (world - 1)
+    if last < 1:
+        raise ValidationError(f"n = {n} too small for {world} ranks with m = {m}")
+    return [q] * (world - 1) + [last]
+
+
+def row_offset(n: int, world: int, m: int, rank: int) -> int:
+    return sum(split_rows(n, world, m)[:rank])
+
+
+class DistributedSolver:
+    """Collective row-sharded solve over an initialised torch.distributed group
+    (backend nccl on GPUs; every rank calls `solve`)."""
+
+    def __init__(self, solver, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.solver = solver
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        dev = torch.device("cuda", solver.device)
+        self.iface = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.iface_all = torch.zeros(8 * self.world, dtype=torch.float64, device=dev)
+
+    def solve(self, a, b, c, d, x, m: int = 10, stream=None):
+        self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
+        self.dist.all_gather_into_tensor(self.iface_all, self.iface, group=self.group)
+        self.solver.dist_solve(a, b, c, d, x, m, self.rank, self.world, self.iface_all, stream=stream)
+        return x

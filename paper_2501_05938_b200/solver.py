@@ -1,0 +1,241 @@
+"""Python host-side mirror of the solver's C ABI (include/pm_tridiag.h).
+
+Same entry points, argument meaning and error behaviour as the C ABI:
+status 1 -> ValidationError, 2 -> ComputationError, 3 -> CudaRuntimeError
+(the streamtune taxonomy, /root/reference/proj/include/streamtune/
+errors.hpp:9-21).  Arrays are float64 numpy arrays (host path) or float64
+CUDA torch tensors (device paths); `a[0]` and `c[n-1]` are ignored.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import ComputationError, CudaRuntimeError, ValidationError, raise_for
+
+PM_OPT_STAGES = 1
+PM_OPT_STREAM_MODE = 2
+PM_OPT_REVERSE_SOLVE = 3
+PM_OPT_MAX_CTAS = 4
+PM_OPT_TIMINGS = 5
+PM_OPT_KERNEL_TIMES = 6
+PM_MAX_M = 128
+
+
+@dataclass
+class StageTimings:
+    """streamtune::StageTimings (timing_model.hpp:77-85), milliseconds."""
+    slae_size: int = 0
+    t1_h2d: float = 0.0
+    t1_comp: float = 0.0
+    t1_d2h: float = 0.0
+    t2_comp: float = 0.0
+    t3_h2d: float = 0.0
+    t3_comp: float = 0.0
+    t3_d2h: float = 0.0
+
+
+def _check_host(*arrs):
+    for x in arrs:
+        if not isinstance(x, np.ndarray) or x.dtype != np.float64 or not x.flags.c_contiguous:
+            raise ValidationError("host arrays must be C-contiguous float64 numpy arrays")
+
+
+def _dev_ptr(t, n: Optional[int] = None) -> int:
+    import torch
+
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
+        raise ValidationError("device arrays must be float64 CUDA tensors")
+    if not t.is_contiguous():
+        raise ValidationError("device arrays must be contiguous")
+    if n is not None and t.numel() < n:
+        raise ValidationError("device array shorter than n")
+    return t.data_ptr()
+
+
+def _stream_handle(stream) -> int:
+    import torch
+
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class PartitionSolver:
+    """One handle per GPU / host thread (pm_create .. pm_destroy)."""
+
+    def __init__(self, device: int = 0, stages: Optional[int] = None, stream_mode: Optional[int] = None,
+                 reverse_solve: Optional[bool] = None, timings: bool = False):
+        self._L = _lib.load()
+        h = C.c_void_p()
+        st = self._L.pm_create(C.byref(h), int(device))
+        if st != 0:
+            raise CudaRuntimeError(f"pm_create failed on device {device} (status {st})")
+        self._h = h
+        self.device = device
+        if stages is not None:
+            self.set_option(PM_OPT_STAGES, stages)
+        if stream_mode is not None:
+            self.set_option(PM_OPT_STREAM_MODE, stream_mode)
+        if reverse_solve is not None:
+            self.set_option(PM_OPT_REVERSE_SOLVE, int(reverse_solve))
+        self.set_option(PM_OPT_TIMINGS, int(timings))
+
+    # -- plumbing -------------------------------------------------------------
+    def _ok(self, st: int):
+        if st != 0:
+            raise_for(st, self._L.pm_last_error(self._h).decode(errors="replace"))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.pm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_option(self, option: int, value: int):
+        self._ok(self._L.pm_set_option(self._h, option, int(value)))
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(self._L.pm_last_launch_count(self._h))
+
+    def last_plan(self) -> list[int]:
+        buf = (C.c_int64 * 16)()
+        k = self._L.pm_last_plan(self._h, buf, 16)
+        return [int(buf[i]) for i in range(min(k, 16))]
+
+    # -- solves -----------------------------------------------------------------
+    def solve_host(self, a, b, c, d, m: int = 10, num_streams: int = 0, out=None) -> np.ndarray:
+        """pm_solve_host_f64: host arrays in, x out (copies overlap compute when
+        the arrays are page-locked, e.g. `pinned_empty`)."""
+        _check_host(a, b, c, d)
+        n = b.shape[0]
+        if not (a.shape[0] == c.shape[0] == d.shape[0] == n):
+            raise ValidationError("a, b, c, d must have the same length")
+        x = out if out is not None else np.empty(n, np.float64)
+        _check_host(x)
+        self._ok(self._L.pm_solve_host_f64(self._h, a.ctypes.data, b.ctypes.data, c.ctypes.data,
+                                           d.ctypes.data, x.ctypes.data, n, m, num_streams))
+        return x
+
+    def solve_device(self, a, b, c, d, m: int = 10, out=None, stream=None, n: Optional[int] = None):
+        """pm_solve_device_f64 (asynchronous; `check()` reports pivot failures)."""
+        import torch
+
+        n = int(b.numel()) if n is None else n
+        x = out if out is not None else torch.empty(n, dtype=torch.float64, device=b.device)
+        self._ok(self._L.pm_solve_device_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
+                                             _dev_ptr(d, n), _dev_ptr(x, n), n, m,
+                                             _stream_handle(stream)))
+        return x
+
+    def solve_batch_device(self, a, b, c, d, n_per_system: int, m: int = 10, out=None, stream=None):
+        import torch
+
+        n = int(b.numel())
+        if n_per_system < 1 or n % n_per_system:
+            raise ValidationError("array length must be a multiple of n_per_system")
+        x = out if out is not None else torch.empty(n, dtype=torch.float64, device=b.device)
+        self._ok(self._L.pm_solve_batch_device_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
+                                                   _dev_ptr(d, n), _dev_ptr(x, n), n_per_system,
+                                                   n // n_per_system, m, _stream_handle(stream)))
+        return x
+
+    def check(self):
+        """pm_check: synchronise and raise ComputationError on a pivot failure."""
+        self._ok(self._L.pm_check(self._h))
+
+    def generate_device(self, n: int, seed: int = 42, device=None, stream=None, arrays=None):
+        """pm_generate_f64 into (new or given) CUDA tensors a, b, c, d."""
+        import torch
+
+        dev = device if device is not None else torch.device("cuda", self.device)
+        if arrays is None:
+            arrays = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(4)]
+        self._ok(self._L.pm_generate_f64(self._h, *[_dev_ptr(t, n) for t in arrays], n, seed,
+                                         _stream_handle(stream)))
+        return arrays
+
+    def generate_range_device(self, n_total: int, row0: int, count: int, seed: int = 42, device=None,
+                              stream=None, arrays=None):
+        """pm_generate_range_f64: rows [row0, row0+count) of the n_total system."""
+        import torch
+
+        dev = device if device is not None else torch.device("cuda", self.device)
+        if arrays is None:
+            arrays = [torch.empty(count, dtype=torch.float64, device=dev) for _ in range(4)]
+        self._ok(self._L.pm_generate_range_f64(self._h, *[_dev_ptr(t, count) for t in arrays], n_total,
+                                               row0, count, seed, _stream_handle(stream)))
+        return arrays
+
+    def kernel_times(self, max_records: int = 65536):
+        """[(mode, level, ms)] recorded while PM_OPT_KERNEL_TIMES is on (synchronises)."""
+        modes = (C.c_int32 * max_records)()
+        levels = (C.c_int32 * max_records)()
+        ms = (C.c_float * max_records)()
+        k = self._L.pm_kernel_times(self._h, modes, levels, ms, max_records)
+        if k < 0:
+            raise CudaRuntimeError(self._L.pm_last_error(self._h).decode())
+        return [(int(modes[i]), int(levels[i]), float(ms[i])) for i in range(k)]
+
+    def last_stage_timings(self):
+        t = _lib.StageTimingsC()
+        total = C.c_double()
+        ns = C.c_int32()
+        self._ok(self._L.pm_last_stage_timings(self._h, C.byref(t), C.byref(total), C.byref(ns)))
+        st = StageTimings(*[getattr(t, f) for f, _ in _lib.StageTimingsC._fields_])
+        return st, total.value, ns.value
+
+    # -- row-sharded single system (BASELINE.json config 5) ---------------------
+    def dist_reduce(self, a, b, c, d, m: int, rank: int, world: int, iface, stream=None):
+        n = int(b.numel())
+        self._ok(self._L.pm_dist_reduce_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
+                                            _dev_ptr(d, n), n, m, rank, world, _dev_ptr(iface, 8),
+                                            _stream_handle(stream)))
+
+    def dist_solve(self, a, b, c, d, x, m: int, rank: int, world: int, iface_all, stream=None):
+        n = int(b.numel())
+        self._ok(self._L.pm_dist_solve_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
+                                           _dev_ptr(d, n), _dev_ptr(x, n), n, m, rank, world,
+                                           _dev_ptr(iface_all, 8 * world), _stream_handle(stream)))
+
+    # -- stream-count model -------------------------------------------------------
+    def set_model_bundle(self, bundle: "ModelBundleC"):
+        self._ok(self._L.pm_set_model_bundle(self._h, C.byref(bundle)))
+
+    def get_model_bundle(self):
+        b = _lib.ModelBundleC()
+        self._ok(self._L.pm_get_model_bundle(self._h, C.byref(b)))
+        return b
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """A page-locked float64 host array (torch's pinned allocator)."""
+    import torch
+
+    return torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+
+
+def recommend_streams(n: int, bundle=None) -> int:
+    L = _lib.load()
+    r = L.pm_recommend_streams(int(n), C.byref(bundle) if bundle is not None else None)
+    if r < 1:
+        raise ValidationError("invalid SLAE size or model bundle")
+    return int(r)

@@ -1,0 +1,276 @@
+"""GPU parity of the partition-method solver against the CPU oracle.
+
+Bars (BASELINE.json north_star): max relative error <= 1e-10 against the
+CPU reference solver on the same inputs, relative residual ||Ax-d||/||d||
+<= 1e-12.  Inputs are the counter-based generator (pm_generate_f64 on the
+device, orc_generate on the host -- bit-identical, checked below).
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-10
+RES_TOL = 1e-12
+
+
+def _device_system(solver, n, seed=42):
+    import torch
+
+    a, b, c, d = solver.generate_device(n, seed)
+    torch.cuda.synchronize()
+    return a, b, c, d
+
+
+def _check(x, a, b, c, d, xref=None):
+    if xref is None:
+        xref = oracle.thomas(a, b, c, d)
+    err = oracle.rel_err(x, xref)
+    res = oracle.residual(a, b, c, d, x)
+    assert err <= REL_TOL, f"rel err {err:.3e}"
+    assert res <= RES_TOL, f"residual {res:.3e}"
+    return err, res
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 64, 1000, 12345])
+def test_generator_bit_identical(solver, n):
+    a, b, c, d = _device_system(solver, n, seed=7)
+    ref = oracle.generate(n, 7)
+    for t, r in zip((a, b, c, d), ref):
+        assert np.array_equal(t.cpu().numpy(), r)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 9, 10, 11, 127, 1279, 1280, 1281, 2559, 2560, 2561, 4097,
+                               100_003, 1_000_007, 3_276_801])
+def test_device_solve_m10(solver, n):
+    a, b, c, d = _device_system(solver, n)
+    x = solver.solve_device(a, b, c, d, m=10)
+    solver.check()
+    _check(x.cpu().numpy(), *oracle.generate(n, 42))
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5, 7, 8, 9, 16, 17, 32, 33, 64, 100, 128])
+@pytest.mark.parametrize("n", [1, 7, 1000, 54_321, 400_000])
+def test_device_solve_m_sweep(solver, m, n):
+    a, b, c, d = _device_system(solver, n, seed=m)
+    x = solver.solve_device(a, b, c, d, m=m)
+    solver.check()
+    _check(x.cpu().numpy(), *oracle.generate(n, m))
+
+
+def test_device_matches_partition_oracle(solver):
+    n, m = 200_000, 10
+    a, b, c, d = _device_system(solver, n)
+    x = solver.solve_device(a, b, c, d, m=m).cpu().numpy()
+    ah, bh, ch, dh = oracle.generate(n, 42)
+    xp = oracle.partition_solve(ah, bh, ch, dh, m)
+    assert oracle.rel_err(x, xp) <= REL_TOL
+
+
+def test_full_size_n8e7(solver):
+    """BASELINE config 3 size: N = 8e7, m = 10, checked against oracle Thomas."""
+    n = 80_000_000
+    a, b, c, d = _device_system(solver, n)
+    x = solver.solve_device(a, b, c, d, m=10)
+    solver.check()
+    xh = x.cpu().numpy()
+    del a, b, c, d, x
+    ah, bh, ch, dh = oracle.generate(n, 42)
+    _check(xh, ah, bh, ch, dh)
+
+
+def test_misaligned_pointers_use_fallback_path(solver):
+    import torch
+
+    n = 50_001
+    ah, bh, ch, dh = oracle.generate(n, 3)
+    bufs = [torch.zeros(n + 1, dtype=torch.float64, device="cuda") for _ in range(5)]
+    for t, h in zip(bufs, (ah, bh, ch, dh)):
+        t[1:].copy_(torch.from_numpy(h))
+    views = [t[1:] for t in bufs]  # 8-byte offset: no 16-byte bulk copies
+    x = solver.solve_device(*views[:4], m=10, out=views[4])
+    solver.check()
+    _check(x.cpu().numpy(), ah, bh, ch, dh)
+
+
+def test_ignored_corners_and_aliasing(solver):
+    import torch
+
+    n = 30_000
+    ah, bh, ch, dh = oracle.generate(n, 5)
+    ref = oracle.thomas(ah, bh, ch, dh)
+    a2, c2 = ah.copy(), ch.copy()
+    a2[0], c2[-1] = 123.0, -77.0  # ignored by contract
+    ta, tb, tc, td = (torch.from_numpy(v.copy()).cuda() for v in (a2, bh, c2, dh))
+    x = solver.solve_device(ta, tb, tc, td, m=10, out=td)  # x aliases d
+    solver.check()
+    assert oracle.rel_err(x.cpu().numpy(), ref) <= REL_TOL
+
+
+@pytest.mark.parametrize("ns", [0, 1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("n", [1000, 1_000_000, 7_654_321])
+def test_host_streams(solver, ns, n):
+    from paper_2501_05938_b200 import pinned_empty
+
+    ah, bh, ch, dh = oracle.generate(n, 11)
+    arrs = []
+    for v in (ah, bh, ch, dh):
+        p = pinned_empty(n)
+        p[:] = v
+        arrs.append(p)
+    x = solver.solve_host(*arrs, m=10, num_streams=ns)
+    _check(x, ah, bh, ch, dh)
+
+
+def test_host_pageable(solver):
+    n = 333_333
+    ah, bh, ch, dh = oracle.generate(n, 12)
+    x = solver.solve_host(ah, bh, ch, dh, m=7, num_streams=4)
+    _check(x, ah, bh, ch, dh)
+
+
+def test_host_stage_timings(solver):
+    from paper_2501_05938_b200 import PM_MAX_M  # noqa: F401
+    from paper_2501_05938_b200.solver import PM_OPT_TIMINGS
+
+    n = 2_000_000
+    ah, bh, ch, dh = oracle.generate(n, 1)
+    solver.set_option(PM_OPT_TIMINGS, 1)
+    try:
+        solver.solve_host(ah, bh, ch, dh, m=10, num_streams=1)
+        st, total, ns = solver.last_stage_timings()
+    finally:
+        solver.set_option(PM_OPT_TIMINGS, 0)
+    assert ns == 1 and st.slae_size == n
+    for f in ("t1_h2d", "t1_comp", "t2_comp", "t3_comp", "t3_d2h"):
+        assert getattr(st, f) > 0.0
+    assert st.t1_d2h == 0.0 and st.t3_h2d == 0.0  # reduced system stays on the device
+    parts = st.t1_h2d + st.t1_comp + st.t2_comp + st.t3_comp + st.t3_d2h
+    assert parts <= total * 1.05 + 0.05
+
+
+@pytest.mark.parametrize("nps,batch,m", [(1000, 16, 10), (100_000, 64, 10), (257, 33, 8), (10, 100, 3)])
+def test_batch(solver, nps, batch, m):
+    import torch
+
+    rng = np.random.default_rng(nps + batch)
+    systems = [oracle.generate(nps, int(s)) for s in rng.integers(0, 2**31, batch)]
+    cat = [np.concatenate([s[k] for s in systems]) for k in range(4)]
+    # the boundary a/c of each system is ignored: poison them
+    for k in range(batch):
+        cat[0][k * nps] = 9.0
+        cat[2][k * nps + nps - 1] = -9.0
+    t = [torch.from_numpy(v).cuda() for v in cat]
+    x = solver.solve_batch_device(*t, n_per_system=nps, m=m).cpu().numpy()
+    solver.check()
+    for k, s in enumerate(systems):
+        _check(x[k * nps:(k + 1) * nps], *s)
+
+
+def test_batch_config4_sample(solver):
+    """BASELINE config 4 on one GPU: 4096 x 1e5, sampled systems checked."""
+    import torch
+
+    nps, batch = 100_000, 4096
+    n = nps * batch
+    a, b, c, d = solver.generate_device(n, 99)
+    x = solver.solve_batch_device(a, b, c, d, n_per_system=nps, m=10)
+    solver.check()
+    ah, bh, ch, dh = (t.cpu().numpy() for t in (a, b, c, d))
+    xh = x.cpu().numpy()
+    del a, b, c, d, x
+    torch.cuda.empty_cache()
+    for k in (0, 1, 777, 2048, 4095):
+        sl = slice(k * nps, (k + 1) * nps)
+        sa, sc = ah[sl].copy(), ch[sl].copy()
+        sa[0] = 0.0
+        sc[-1] = 0.0
+        _check(xh[sl], sa, bh[sl].copy(), sc, dh[sl].copy())
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("n,m", [(1_000_000, 10), (77_777, 7), (4_000, 10)])
+def test_dist_virtual_ranks(solver, world, n, m):
+    """Row-sharded solve with `world` virtual ranks on one GPU; the allgather
+    is a device copy (the NCCL path is exercised by bench.py under torchrun)."""
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.dist import split_rows
+
+    # one handle per rank, as one process per GPU would have: a handle's
+    # level scratch carries state from dist_reduce to dist_solve
+    handles = [solver] + [PartitionSolver(0) for _ in range(world - 1)]
+    ah, bh, ch, dh = oracle.generate(n, 21)
+    rows = split_rows(n, world, m)
+    assert sum(rows) == n
+    offs = np.concatenate([[0], np.cumsum(rows)])
+    loc = [[torch.from_numpy(v[offs[r]:offs[r + 1]].copy()).cuda() for v in (ah, bh, ch, dh)]
+           for r in range(world)]
+    iface_all = torch.zeros(8 * world, dtype=torch.float64, device="cuda")
+    for r in range(world):
+        handles[r].dist_reduce(*loc[r], m=m, rank=r, world=world, iface=iface_all[8 * r:8 * r + 8])
+    xs = []
+    for r in range(world):
+        x = torch.empty(rows[r], dtype=torch.float64, device="cuda")
+        handles[r].dist_solve(*loc[r], x, m=m, rank=r, world=world, iface_all=iface_all)
+        xs.append(x)
+    for h in handles:
+        h.check()
+    for h in handles[1:]:
+        h.close()
+    _check(torch.cat(xs).cpu().numpy(), ah, bh, ch, dh)
+
+
+def test_validation_errors(solver):
+    import torch
+
+    from paper_2501_05938_b200 import InvalidStreamCountError, ValidationError
+
+    t = [torch.ones(10, dtype=torch.float64, device="cuda") for _ in range(4)]
+    with pytest.raises(ValidationError):
+        solver.solve_device(*t, m=1)
+    with pytest.raises(ValidationError):
+        solver.solve_device(*t, m=129)
+    with pytest.raises(ValidationError):
+        solver.solve_device(*t, m=10, n=0)
+    h = [np.ones(10) for _ in range(4)]
+    with pytest.raises(InvalidStreamCountError):
+        solver.solve_host(*h, m=10, num_streams=3)
+    with pytest.raises(InvalidStreamCountError):
+        solver.solve_host(*h, m=10, num_streams=64)
+
+
+def test_zero_pivot_is_computation_error(solver):
+    import torch
+
+    from paper_2501_05938_b200 import ComputationError
+
+    n = 5000
+    ah, bh, ch, dh = oracle.generate(n, 4)
+    bh = bh.copy()
+    ah, ch = ah.copy(), ch.copy()
+    ah[1234] = ch[1234] = bh[1234] = 0.0  # an all-zero row: singular
+    t = [torch.from_numpy(v).cuda() for v in (ah, bh, ch, dh)]
+    solver.solve_device(*t, m=10)
+    with pytest.raises(ComputationError):
+        solver.check()
+    # the flag was cleared: a good solve afterwards passes
+    a, b, c, d = _device_system(solver, 1000)
+    solver.solve_device(a, b, c, d, m=10)
+    solver.check()
+
+
+def test_launch_plan_n8e7(solver):
+    import torch
+
+    n = 80_000_000
+    a = torch.empty(n, dtype=torch.float64, device="cuda")
+    b, c, d = torch.empty_like(a), torch.empty_like(a), torch.empty_like(a)
+    solver.generate_device(n, 1, arrays=[a, b, c, d])
+    solver.solve_device(a, b, c, d, m=10)
+    solver.check()
+    assert solver.last_plan() == [80_000_000, 125_000, 246]
+    assert solver.last_launch_count == 5
