@@ -84,6 +84,8 @@ typedef struct pm_model_bundle {
                                   pm_solve_host_f64 (num_streams == 1 only)        */
 #define PM_OPT_KERNEL_TIMES 6  /* 1: bracket every kernel launch with CUDA events;
                                   read them with pm_kernel_times                   */
+#define PM_OPT_WARP_TILES 7    /* 1 (default): level 0 uses warp-owned tiles of
+                                  32*m rows; 0: CTA tiles (P*m rows, P <= 128)     */
 
 int pm_create(pm_handle_t* out, int device);
 int pm_destroy(pm_handle_t h);

@@ -46,6 +46,7 @@ struct Level {
   bool bulk = true;
   int pad_mode = 1;
   int stages = 2;
+  int warps_per_cta = 0;  // > 0: warp-tile kernel (P = 32 rows-blocks per tile)
 };
 
 constexpr size_t kSmemLimit = 226 * 1024;
@@ -70,6 +71,7 @@ struct pm_handle_s {
   int reverse = 1;
   int max_ctas = 0;
   int timings = 0;
+  int warp_tiles = 1;
   // device scratch for upper levels (+ dist boundary values)
   double* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -139,15 +141,32 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   Level L0;
   L0.n = n;
   L0.m = m;
-  L0.P = choose_P(m);
-  L0.T = (int64_t)L0.P * m;
-  L0.ntiles = (n + L0.T - 1) / L0.T;
   L0.a = a; L0.b = b; L0.c = c; L0.d = d; L0.x = x;
   L0.pad_mode = ragged0 ? 0 : 1;
-  L0.stages = pick_stages(h->stages, L0.P, m);
-  if (pm::tile_smem_bytes(pm::kModeSolve, L0.P, m, 1) > kSmemLimit)
-    return fail(h, PM_ERR_VALIDATION, "sub-system size m too large for shared memory");
   L0.bulk = aligned16(a) && aligned16(b) && aligned16(c) && aligned16(d) && aligned16(x);
+  if (L0.bulk && h->warp_tiles) {
+    // warp tiles: as many warps per CTA (<= 4) as the shared memory allows
+    int S = std::max(1, std::min(h->stages, 4));
+    int W = 0;
+    while (S >= 1) {
+      W = (int)std::min<size_t>(4, kSmemLimit / pm::warp_smem_bytes(pm::kModeSolve, m, S));
+      if (W >= 1) break;
+      --S;
+    }
+    if (W >= 1) {
+      L0.P = 32;
+      L0.stages = S;
+      L0.warps_per_cta = W;
+    }
+  }
+  if (L0.warps_per_cta == 0) {
+    L0.P = choose_P(m);
+    L0.stages = pick_stages(h->stages, L0.P, m);
+    if (pm::tile_smem_bytes(pm::kModeSolve, L0.P, m, 1) > kSmemLimit)
+      return fail(h, PM_ERR_VALIDATION, "sub-system size m too large for shared memory");
+  }
+  L0.T = (int64_t)L0.P * m;
+  L0.ntiles = (n + L0.T - 1) / L0.T;
   lv.push_back(L0);
   while (lv.back().ntiles > 1) {
     const Level& prev = lv.back();
@@ -214,7 +233,11 @@ int launch(pm_handle_t h, int mode, const TileArgs& A, const Level& L, cudaStrea
   const bool timed = h->ktimes && next_kevent(h) != nullptr;
   const size_t ev = h->krec.size() * 2;
   if (timed) cudaEventRecord(h->kev[ev], st);
-  cudaError_t e = pm::launch_tile_kernel(mode, A, L.P, L.bulk, h->sm_count, st, &grid);
+  cudaError_t e;
+  if (L.warps_per_cta > 0 && mode != pm::kModeRoot)
+    e = pm::launch_warp_tile_kernel(mode, A, L.warps_per_cta, h->sm_count, st, &grid);
+  else
+    e = pm::launch_tile_kernel(mode, A, L.P, L.bulk, h->sm_count, st, &grid);
   if (e != cudaSuccess) return cuda_fail(h, e, "tile kernel launch");
   if (timed) {
     cudaEventRecord(h->kev[ev + 1], st);
@@ -387,6 +410,9 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       return PM_OK;
     case PM_OPT_TIMINGS:
       h->timings = value ? 1 : 0;
+      return PM_OK;
+    case PM_OPT_WARP_TILES:
+      h->warp_tiles = value ? 1 : 0;
       return PM_OK;
     case PM_OPT_KERNEL_TIMES:
       h->ktimes = value ? 1 : 0;

@@ -35,7 +35,22 @@ struct Node {
   double p0, p1, p2, q0, q1, q2;
 };
 
-__device__ __forceinline__ double drcp(double x) { return __drcp_rn(x); }
+// Reciprocal on the dependency chain of every sweep: the MUFU seed
+// (rcp.approx.ftz.f64) refined by two Newton steps (<= 1 ulp), instead of the
+// IEEE-rounded __drcp_rn sequence with its slow-path branch.  A zero pivot
+// still yields inf/NaN (and is flagged separately).
+__device__ __forceinline__ double drcp(double x) {
+#ifdef PM_EXACT_RCP
+  return __drcp_rn(x);
+#else
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#endif
+}
 
 // Merge segment A = [f1..l1] with its right neighbour B = [f2..l2], f2 = l1+1,
 // eliminating x[l1] and x[f2].

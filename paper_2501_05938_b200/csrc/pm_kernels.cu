@@ -504,6 +504,215 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
 }
 
 // ---------------------------------------------------------------------------
+// Warp-tile kernel (level 0).  "One warp per group of blocks" (north_star):
+// a tile is 32 m-blocks = 32*m rows owned by one warp, with a private ring of
+// `stages` shared-memory buffers and mbarriers.  Warps never synchronise with
+// each other, so the FP64 dependency chains of the sweeps and the combine
+// tree of one warp overlap with every other warp on the SM; loads for the
+// warp's next tiles are in flight while it computes.  The tile's reduced rows
+// go to the level above, which uses the CTA-tile kernel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ Seg warp_upsweep(Seg s, Node* nodes, int lane, int nblk, bool& bad) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int stride = 1 << k;
+    Seg o = shfl_down_seg(s, stride);
+    if ((lane & (2 * stride - 1)) == 0 && lane + stride < nblk) {
+      Node nd;
+      combine(s, o, s, nd, bad);
+      if (nodes) nodes[warp_node_off(k) + (lane >> (k + 1))] = nd;
+    }
+  }
+  return s;
+}
+
+__device__ __forceinline__ void warp_downsweep(double& xf, double& xl, const Node* nodes, int lane,
+                                               int nblk) {
+#pragma unroll
+  for (int k = 4; k >= 0; --k)
+    down_level(nodes + warp_node_off(k), 1 << k, lane, 32, lane + (1 << k) < nblk, xf, xl);
+}
+
+__host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages) {
+  const size_t T = (size_t)32 * m;
+  size_t bytes = (size_t)stages * 4 * T * sizeof(double) + 2 * kMaxStages * sizeof(uint64_t);
+  if (mode != kModeReduce) bytes += T * sizeof(double) + 31 * sizeof(Node);
+  return (bytes + 127) / 128 * 128;
+}
+
+template <int M, int MODE>
+__global__ void __launch_bounds__(128) warp_tile_kernel(TileArgs args) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int m = (M > 0) ? M : args.m;
+  const int T = 32 * m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int S = args.stages;
+  const int r0 = lane * m;
+  const size_t per_warp = warp_smem_bytes(MODE, m, S);
+  unsigned char* base = smem_raw + per_warp * warp;
+  double* stage0 = reinterpret_cast<double*>(base);
+  double* xbuf = stage0 + (size_t)S * 4 * T;
+  Node* nodes = reinterpret_cast<Node*>(xbuf + T);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + per_warp - 2 * kMaxStages * sizeof(uint64_t));
+
+  const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int64_t nwarp_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t ntiles = args.tile_end - args.tile_begin;
+  const int64_t nlocal = (ntiles > gwarp) ? (ntiles - gwarp + nwarp_total - 1) / nwarp_total : 0;
+  auto tile_of = [&](int64_t k) -> int64_t {
+    const int64_t idx = gwarp + k * nwarp_total;
+    return args.reverse ? (args.tile_end - 1 - idx) : (args.tile_begin + idx);
+  };
+  auto stage_ptr = [&](int s, int q) -> double* { return stage0 + ((size_t)s * 4 + q) * T; };
+  auto issue = [&](int s, int64_t t) {
+    const int64_t row0 = t * T;
+    const int64_t v = (args.n - row0 < T) ? (args.n - row0) : T;
+    const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(1)) * 8);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&bars[s], 4u * bytes);
+    if (bytes) {
+      bulk_g2s(stage_ptr(s, 0), args.a + row0, bytes, &bars[s]);
+      bulk_g2s(stage_ptr(s, 1), args.b + row0, bytes, &bars[s]);
+      bulk_g2s(stage_ptr(s, 2), args.c + row0, bytes, &bars[s]);
+      bulk_g2s(stage_ptr(s, 3), args.d + row0, bytes, &bars[s]);
+    }
+  };
+
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int s = 0; s < S && s < nlocal; ++s) issue(s, tile_of(s));
+
+  bool bad = false;
+  for (int64_t k = 0; k < nlocal; ++k) {
+    const int64_t t = tile_of(k);
+    const int s = static_cast<int>(k % S);
+    TileCtx ctx;
+    ctx.ga = args.a; ctx.gb = args.b; ctx.gc = args.c; ctx.gd = args.d;
+    ctx.row0 = t * T;
+    ctx.n = args.n;
+    ctx.valid = static_cast<int>((args.n - ctx.row0 < T) ? (args.n - ctx.row0) : T);
+    ctx.odd_tail = (ctx.valid & 1);
+    ctx.zf = args.zero_first != 0;
+    ctx.zl = args.zero_last != 0;
+    ctx.sys_len = args.sys_len;
+    const int nblk = args.pad_mode ? 32 : (ctx.valid + m - 1) / m;
+    double* sa = stage_ptr(s, 0);
+    double* sb = stage_ptr(s, 1);
+    double* sc = stage_ptr(s, 2);
+    double* sd = stage_ptr(s, 3);
+    mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
+
+    Seg seg;
+    RegAcc<(M > 0 ? M : 1)> regs;
+    SmemAcc sacc{sa + r0, sb + r0, sc + r0, sd + r0, xbuf + r0};
+    if constexpr (M > 0) {
+      regs.load(sa, sb, sc, sd, r0, ctx);
+      __syncwarp();
+      if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));  // early release
+      seg = block_reduce<M>(regs, m, bad);
+    } else {
+      sacc.fixup(r0, m, ctx);
+      seg = block_reduce<0>(sacc, m, bad);
+      if constexpr (MODE == kModeReduce) {
+        __syncwarp();
+        if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));
+      }
+    }
+
+    Seg top = warp_upsweep(seg, MODE == kModeReduce ? nullptr : nodes, lane, nblk, bad);
+    if constexpr (MODE == kModeReduce) {
+      if (lane == 0) {
+        args.ra[2 * t] = top.F.a; args.rb[2 * t] = top.F.b;
+        args.rc[2 * t] = top.F.c; args.rd[2 * t] = top.F.d;
+        args.ra[2 * t + 1] = top.L.a; args.rb[2 * t + 1] = top.L.b;
+        args.rc[2 * t + 1] = top.L.c; args.rd[2 * t + 1] = top.L.d;
+      }
+    } else {
+      double xf = __ldg(args.xb + 2 * t), xl = __ldg(args.xb + 2 * t + 1);
+      __syncwarp();  // nodes written by lanes are read by the same lanes only
+      warp_downsweep(xf, xl, nodes, lane, nblk);
+      if constexpr (M > 0) {
+        block_interior<M>(regs, m, xf, xl, bad);
+#pragma unroll
+        for (int j = 0; j < M; ++j) bad |= !isfinite(regs.x(j));
+        regs.store_x(xbuf, r0);
+      } else {
+        block_interior<0>(sacc, m, xf, xl, bad);
+        for (int j = 0; j < m; ++j) bad |= !isfinite(sacc.x(j));
+      }
+      __syncwarp();
+      // coalesced store of the tile's x
+      double* gx = args.x + ctx.row0;
+      const int v = ctx.valid;
+      if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & 15) == 0)) {
+        const double2* s2 = reinterpret_cast<const double2*>(xbuf);
+        double2* g2 = reinterpret_cast<double2*>(gx);
+        for (int i = lane; i < v / 2; i += 32) g2[i] = s2[i];
+      } else {
+        for (int i = lane; i < v; i += 32) gx[i] = xbuf[i];
+      }
+      __syncwarp();
+      if constexpr (M == 0) {
+        if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));
+      }
+    }
+  }
+  if (bad) atomicOr(args.flag, 1);
+}
+
+template <int M, int MODE>
+static cudaError_t launch_warp_one(const TileArgs& args, int warps_per_cta, int sm_count,
+                                   cudaStream_t st, int* grid_out) {
+  auto kern = warp_tile_kernel<M, MODE>;
+  const int m = (M > 0 ? M : args.m);
+  const size_t smem = warp_smem_bytes(MODE, m, args.stages) * warps_per_cta;
+  static thread_local size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta,
+                                                                smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int64_t ntiles = args.tile_end - args.tile_begin;
+  int64_t grid = (int64_t)per_sm * sm_count;
+  if (args.max_ctas > 0 && grid > args.max_ctas) grid = args.max_ctas;
+  const int64_t need = (ntiles + warps_per_cta - 1) / warps_per_cta;
+  if (grid > need) grid = need;
+  if (grid_out) *grid_out = (int)grid;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<(unsigned)grid, 32 * warps_per_cta, smem, st>>>(args);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_warp_tile_kernel(int mode, const TileArgs& args, int warps_per_cta,
+                                    int sm_count, cudaStream_t st, int* grid_out) {
+  const bool red = (mode == kModeReduce);
+  switch (m_is_specialised(args.m) ? args.m : 0) {
+    case 2:
+      return red ? launch_warp_one<2, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
+                 : launch_warp_one<2, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
+    case 8:
+      return red ? launch_warp_one<8, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
+                 : launch_warp_one<8, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
+    case 10:
+      return red ? launch_warp_one<10, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
+                 : launch_warp_one<10, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
+    default:
+      return red ? launch_warp_one<0, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
+                 : launch_warp_one<0, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Row-sharded solve: the 2*world-row interface system, solved redundantly by
 // one thread on every rank.  Segment k = rank k's two
 // interface equations; chain-combine 0..world-1 keeping the nodes, solve the

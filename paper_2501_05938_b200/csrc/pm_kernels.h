@@ -45,6 +45,11 @@ cudaError_t launch_dist_chain(const double* iface_all, int world, int rank, doub
                               cudaStream_t st);
 
 size_t tile_smem_bytes(int mode, int P, int m, int stages);
+// Level-0 warp-tile kernel: a tile is 32*m rows owned by one warp (REDUCE or
+// SOLVE; 16-byte aligned arrays only).  Shared memory per warp:
+__host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages);
+cudaError_t launch_warp_tile_kernel(int mode, const TileArgs& args, int warps_per_cta,
+                                    int sm_count, cudaStream_t st, int* grid_out);
 bool m_is_specialised(int m);
 cudaError_t launch_tile_kernel(int mode, const TileArgs& args, int P, bool bulk, int sm_count,
                                cudaStream_t st, int* grid_out);

@@ -23,6 +23,7 @@ PM_OPT_REVERSE_SOLVE = 3
 PM_OPT_MAX_CTAS = 4
 PM_OPT_TIMINGS = 5
 PM_OPT_KERNEL_TIMES = 6
+PM_OPT_WARP_TILES = 7
 PM_MAX_M = 128
 
 

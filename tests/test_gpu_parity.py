@@ -272,5 +272,24 @@ def test_launch_plan_n8e7(solver):
     solver.generate_device(n, 1, arrays=[a, b, c, d])
     solver.solve_device(a, b, c, d, m=10)
     solver.check()
-    assert solver.last_plan() == [80_000_000, 125_000, 246]
+    # level 0: warp tiles of 32*10 rows -> 2 rows each; level 1: CTA tiles of 1024 rows
+    assert solver.last_plan() == [80_000_000, 500_000, 978]
     assert solver.last_launch_count == 5
+
+
+@pytest.mark.parametrize("warp_tiles", [0, 1])
+@pytest.mark.parametrize("n,m", [(1, 10), (319, 10), (320, 10), (321, 10), (1_234_567, 10), (99_999, 8),
+                                 (65_536, 2), (300_001, 5), (12_345, 128)])
+def test_level0_kernel_variants(solver, warp_tiles, n, m):
+    from paper_2501_05938_b200.solver import PM_OPT_WARP_TILES
+
+    solver.set_option(PM_OPT_WARP_TILES, warp_tiles)
+    try:
+        a, b, c, d = _device_system(solver, n, seed=n % 97)
+        x = solver.solve_device(a, b, c, d, m=m)
+        solver.check()
+        plan = solver.last_plan()
+        assert solver.last_launch_count == 2 * len(plan) - 1
+    finally:
+        solver.set_option(PM_OPT_WARP_TILES, 1)
+    _check(x.cpu().numpy(), *oracle.generate(n, n % 97))
