@@ -145,6 +145,81 @@ __device__ __forceinline__ Seg block_reduce(const Acc& r, int m_rt, bool& bad) {
   return S;
 }
 
+// Stage 1 for Stage 3's benefit: as block_reduce, but the forward sweep's
+// reciprocals and c' are kept in the row storage (b(j) <- 1/den_j,
+// c(j) <- c'_j for interior j < L; c(L) keeps c_{e-1}) so that
+// block_interior_kept needs no reciprocal on its dependency chain.
+template <int M, class Acc>
+__device__ __forceinline__ Seg block_reduce_keep(Acc& r, bool& bad) {
+  static_assert(M > 0, "compile-time m only");
+  Seg S;
+  if constexpr (M == 2) {
+    S.F = Row{r.a(0), r.b(0), r.c(0), r.d(0)};
+    S.L = Row{r.a(1), r.b(1), r.c(1), r.d(1)};
+    return S;
+  } else {
+    constexpr int L = M - 2;
+    double den = r.b(1);
+    bad |= (den == 0.0);
+    double inv = drcp(den);
+    double cp = (L > 1) ? r.c(1) * inv : 0.0;
+    double yp = r.d(1) * inv;
+    double gp = r.a(1) * inv;
+    double P = 1.0, Y1 = yp, G1 = gp;
+    r.B[1] = inv;
+    if (L > 1) r.C[1] = cp;
+#pragma unroll
+    for (int j = 2; j <= L; ++j) {
+      const double aj = r.a(j);
+      den = fma(-aj, cp, r.b(j));
+      bad |= (den == 0.0);
+      inv = drcp(den);
+      P = -P * cp;
+      yp = fma(-aj, yp, r.d(j)) * inv;
+      gp = -aj * gp * inv;
+      cp = (j < L) ? r.c(j) * inv : 0.0;
+      Y1 = fma(P, yp, Y1);
+      G1 = fma(P, gp, G1);
+      r.B[j] = inv;
+      if (j < L) r.C[j] = cp;
+    }
+    const double hL = r.c(L) * inv;
+    const double H1 = P * hL;
+    const double as = r.a(0), bs = r.b(0), cs = r.c(0), ds = r.d(0);
+    const double ae = r.a(M - 1), be = r.b(M - 1), ce = r.c(M - 1), de = r.d(M - 1);
+    S.F = Row{as, fma(-cs, G1, bs), -cs * H1, fma(-cs, Y1, ds)};
+    S.L = Row{-ae * gp, fma(-ae, hL, be), ce, fma(-ae, yp, de)};
+    return S;
+  }
+}
+
+// Stage 3 after block_reduce_keep: forward substitution with the stored
+// reciprocals (an FMA + MUL chain per row), then back-substitution; x is
+// written over b(j).
+template <int M, class Acc>
+__device__ __forceinline__ void block_interior_kept(Acc& r, double xs, double xe) {
+  if constexpr (M == 2) {
+    r.B[0] = xs;
+    r.B[1] = xe;
+  } else {
+    constexpr int L = M - 2;
+    double dp[L + 1];
+    dp[1] = fma(-r.a(1), xs, r.d(1)) * r.B[1];
+#pragma unroll
+    for (int j = 2; j <= L; ++j) dp[j] = fma(-r.a(j), dp[j - 1], r.d(j)) * r.B[j];
+    dp[L] = fma(-(r.C[L] * r.B[L]), xe, dp[L]);  // - h_L * x_e
+    double xn = dp[L];
+    r.B[L] = xn;
+#pragma unroll
+    for (int j = L - 1; j >= 1; --j) {
+      xn = fma(-r.C[j], xn, dp[j]);
+      r.B[j] = xn;
+    }
+    r.B[0] = xs;
+    r.B[M - 1] = xe;
+  }
+}
+
 // Stage 3 for one block: Thomas on the interior with known x[s] = xs and
 // x[e] = xe folded into the right-hand side.  Writes x(j) for j = 0..m-1
 // through r.set_x.  Acc must also provide scratch set_cp/cp, set_dp/dp.

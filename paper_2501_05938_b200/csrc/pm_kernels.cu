@@ -587,9 +587,23 @@ __global__ void __launch_bounds__(128) warp_tile_kernel(TileArgs args) {
     for (int s = 0; s < S && s < nlocal; ++s) issue(s, tile_of(s));
 
   bool bad = false;
+  // Stage 3: the tile's boundary values come from the level above; fetch
+  // them one tile ahead so the load latency is off the critical path.
+  double xf_next = 0.0, xl_next = 0.0;
+  if (MODE != kModeReduce && nlocal > 0) {
+    const int64_t t0 = tile_of(0);
+    xf_next = __ldg(args.xb + 2 * t0);
+    xl_next = __ldg(args.xb + 2 * t0 + 1);
+  }
   for (int64_t k = 0; k < nlocal; ++k) {
     const int64_t t = tile_of(k);
     const int s = static_cast<int>(k % S);
+    double xf_tile = xf_next, xl_tile = xl_next;
+    if (MODE != kModeReduce && k + 1 < nlocal) {
+      const int64_t tn = tile_of(k + 1);
+      xf_next = __ldg(args.xb + 2 * tn);
+      xl_next = __ldg(args.xb + 2 * tn + 1);
+    }
     TileCtx ctx;
     ctx.ga = args.a; ctx.gb = args.b; ctx.gc = args.c; ctx.gd = args.d;
     ctx.row0 = t * T;
@@ -613,7 +627,10 @@ __global__ void __launch_bounds__(128) warp_tile_kernel(TileArgs args) {
       regs.load(sa, sb, sc, sd, r0, ctx);
       __syncwarp();
       if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));  // early release
-      seg = block_reduce<M>(regs, m, bad);
+      if constexpr (MODE == kModeReduce)
+        seg = block_reduce<M>(regs, m, bad);
+      else
+        seg = block_reduce_keep<M>(regs, bad);
     } else {
       sacc.fixup(r0, m, ctx);
       seg = block_reduce<0>(sacc, m, bad);
@@ -632,11 +649,11 @@ __global__ void __launch_bounds__(128) warp_tile_kernel(TileArgs args) {
         args.rc[2 * t + 1] = top.L.c; args.rd[2 * t + 1] = top.L.d;
       }
     } else {
-      double xf = __ldg(args.xb + 2 * t), xl = __ldg(args.xb + 2 * t + 1);
+      double xf = xf_tile, xl = xl_tile;
       __syncwarp();  // nodes written by lanes are read by the same lanes only
       warp_downsweep(xf, xl, nodes, lane, nblk);
       if constexpr (M > 0) {
-        block_interior<M>(regs, m, xf, xl, bad);
+        block_interior_kept<M>(regs, xf, xl);
 #pragma unroll
         for (int j = 0; j < M; ++j) bad |= !isfinite(regs.x(j));
         regs.store_x(xbuf, r0);
