@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--num-streams", type=int, default=0, help="e2e stream count (0 = predictor)")
+    p.add_argument("--opt", action="append", default=[],
+                   help="solver option NAME=VALUE (PM_OPT_* without the prefix), experiments")
     return p.parse_args()
 
 
@@ -211,6 +213,10 @@ def main():
     row0 = sum(rows[:rank])
 
     solver = PartitionSolver(local)
+    import paper_2501_05938_b200.solver as _solver_mod
+    for kv in args.opt:
+        name, val = kv.split("=")
+        solver.set_option(getattr(_solver_mod, "PM_OPT_" + name.upper()), int(val))
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     with torch.cuda.stream(stream):

@@ -86,6 +86,9 @@ typedef struct pm_model_bundle {
                                   read them with pm_kernel_times                   */
 #define PM_OPT_WARP_TILES 7    /* 1 (default): level 0 uses warp-owned tiles of
                                   32*m rows; 0: CTA tiles (P*m rows, P <= 128)     */
+#define PM_OPT_SOLVE_STAGES 8  /* ring depth of the level-0 Stage-3 kernel
+                                  (0 = PM_OPT_STAGES)                              */
+#define PM_OPT_WARPS_PER_CTA 9 /* warps per CTA of the warp-tile kernels (1..8)    */
 
 int pm_create(pm_handle_t* out, int device);
 int pm_destroy(pm_handle_t h);

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libpm_tridiag.so"
+LIB_PATH = Path(os.environ.get("PM_LIB_PATH") or Path(__file__).resolve().parent / "libpm_tridiag.so")
 
 _D = C.POINTER(C.c_double)
 _CD = C.c_void_p  # device / host pointers are passed as integers

@@ -20,6 +20,8 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 BUILD = ROOT / "build" / "obj"
 LIB = PKG / "libpm_tridiag.so"
+# extra nvcc flags (experiments only), e.g. PM_NVCC_FLAGS="-DPM_SOLVE_MINB=3"
+EXTRA = os.environ.get("PM_NVCC_FLAGS", "").split()
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -47,7 +49,7 @@ def _compile(src: Path) -> Path:
     newest_dep = max([src.stat().st_mtime] + [h.stat().st_mtime for h in headers()])
     if obj.exists() and obj.stat().st_mtime >= newest_dep:
         return obj
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", *EXTRA,
            f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -55,7 +57,11 @@ def _compile(src: Path) -> Path:
     return obj
 
 
-def build(verbose: bool = False) -> Path:
+def build(verbose: bool = False, out: Path | None = None) -> Path:
+    global BUILD, LIB
+    if out is not None:  # variant build (experiments): separate objects and library
+        BUILD = ROOT / "build" / ("obj_" + out.stem)
+        LIB = out
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(_compile, srcs))
@@ -74,4 +80,4 @@ def build(verbose: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(verbose=True)
+    build(verbose=True, out=Path(sys.argv[1]).resolve() if len(sys.argv) > 1 else None)

@@ -72,6 +72,8 @@ struct pm_handle_s {
   int max_ctas = 0;
   int timings = 0;
   int warp_tiles = 1;
+  int solve_stages = 0;   // 0 = same as `stages`
+  int warps_per_cta = 4;
   // device scratch for upper levels (+ dist boundary values)
   double* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -146,10 +148,11 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   L0.bulk = aligned16(a) && aligned16(b) && aligned16(c) && aligned16(d) && aligned16(x);
   if (L0.bulk && h->warp_tiles) {
     // warp tiles: as many warps per CTA (<= 4) as the shared memory allows
-    int S = std::max(1, std::min(h->stages, 4));
+    int S = std::max(1, std::min(std::max(h->stages, h->solve_stages), 4));
     int W = 0;
     while (S >= 1) {
-      W = (int)std::min<size_t>(4, kSmemLimit / pm::warp_smem_bytes(pm::kModeSolve, m, S));
+      W = (int)std::min<size_t>(h->warps_per_cta,
+                                kSmemLimit / pm::warp_smem_bytes(pm::kModeSolve, m, S));
       if (W >= 1) break;
       --S;
     }
@@ -270,6 +273,7 @@ int enq_solve(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, 
   const Level& L = h->levels[k];
   TileArgs A = args_for(h, L, t0, t1);
   A.xb = xb ? xb : h->levels[k + 1].x;
+  if (L.warps_per_cta > 0 && h->solve_stages > 0) A.stages = std::min(h->solve_stages, L.stages);
   A.zero_first = zf;
   A.zero_last = zl;
   A.sys_len = (k == 0) ? sys_len : 0;
@@ -413,6 +417,14 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       return PM_OK;
     case PM_OPT_WARP_TILES:
       h->warp_tiles = value ? 1 : 0;
+      return PM_OK;
+    case PM_OPT_SOLVE_STAGES:
+      if (value < 0 || value > 4) return fail(h, PM_ERR_VALIDATION, "solve stages must lie in [0, 4]");
+      h->solve_stages = (int)value;
+      return PM_OK;
+    case PM_OPT_WARPS_PER_CTA:
+      if (value < 1 || value > 8) return fail(h, PM_ERR_VALIDATION, "warps per CTA must lie in [1, 8]");
+      h->warps_per_cta = (int)value;
       return PM_OK;
     case PM_OPT_KERNEL_TIMES:
       h->ktimes = value ? 1 : 0;

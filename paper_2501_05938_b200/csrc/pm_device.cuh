@@ -29,16 +29,17 @@ struct Row {
 struct Seg {
   Row F, L;
 };
-// Junction solve of a combine:  x[l1] = p0 + p1*x[f1] + p2*x[l2]
-//                               x[f2] = q0 + q1*x[f1] + q2*x[l2]
+// Junction solve of a combine (scaled by r = 1 / (s * det)):
+//   x[l1] = (p0 + p1*x[f1] + p2*x[l2]) * r
+//   x[f2] = (q0 + q1*x[f1] + q2*x[l2]) * r
 struct Node {
-  double p0, p1, p2, q0, q1, q2;
+  double p0, p1, p2, q0, q1, q2, r;
 };
 
-// Reciprocal on the dependency chain of every sweep: the MUFU seed
-// (rcp.approx.ftz.f64) refined by two Newton steps (<= 1 ulp), instead of the
-// IEEE-rounded __drcp_rn sequence with its slow-path branch.  A zero pivot
-// still yields inf/NaN (and is flagged separately).
+// Reciprocal: the MUFU seed (rcp.approx.ftz.f64) refined by two Newton steps
+// (<= 1 ulp), instead of the IEEE-rounded __drcp_rn sequence with its
+// slow-path branch.  A zero argument yields inf/NaN (and is flagged
+// separately by the callers).
 __device__ __forceinline__ double drcp(double x) {
 #ifdef PM_EXACT_RCP
   return __drcp_rn(x);
@@ -52,29 +53,52 @@ __device__ __forceinline__ double drcp(double x) {
 #endif
 }
 
+// 2^-(e(u) + e(v)), e = unbiased binary exponent: an exact power-of-two
+// scale that keeps u*v-sized products near 1 (clamped to the normal range).
+__device__ __forceinline__ double pow2_inv_scale(double u, double v) {
+  const int eu = (__double2hiint(u) >> 20) & 0x7ff;
+  const int ev = (__double2hiint(v) >> 20) & 0x7ff;
+  int e = eu + ev - 2 * 1023;
+  e = max(-1000, min(1000, e));
+  return __hiloint2double((1023 - e) << 20, 0);
+}
+
 // Merge segment A = [f1..l1] with its right neighbour B = [f2..l2], f2 = l1+1,
-// eliminating x[l1] and x[f2].
+// eliminating x[l1] and x[f2].  Division-free: both output equations are
+// multiplied by s*det (equations may be scaled freely), with s an exact
+// power of two chosen from the operands' exponents before det is known, so
+// the upsweep's dependency chain is four FP64 operations per level; the
+// reciprocal the downsweep needs is computed off that chain.
 __device__ __forceinline__ void combine(const Seg& A, const Seg& B, Seg& out, Node& nd,
                                         bool& bad) {
+  const double s = pow2_inv_scale(A.L.b, B.F.b);
   const double det = fma(A.L.b, B.F.b, -A.L.c * B.F.a);
   bad |= (det == 0.0);
-  const double inv = drcp(det);
-  nd.p0 = fma(B.F.b, A.L.d, -A.L.c * B.F.d) * inv;
-  nd.p1 = -(B.F.b * A.L.a) * inv;
-  nd.p2 = (A.L.c * B.F.c) * inv;
-  nd.q0 = fma(A.L.b, B.F.d, -B.F.a * A.L.d) * inv;
-  nd.q1 = (B.F.a * A.L.a) * inv;
-  nd.q2 = -(A.L.b * B.F.c) * inv;
+  const double ds = det * s;
+  nd.p0 = fma(B.F.b, A.L.d, -A.L.c * B.F.d) * s;
+  nd.p1 = -(B.F.b * A.L.a) * s;
+  nd.p2 = (A.L.c * B.F.c) * s;
+  nd.q0 = fma(A.L.b, B.F.d, -B.F.a * A.L.d) * s;
+  nd.q1 = (B.F.a * A.L.a) * s;
+  nd.q2 = -(A.L.b * B.F.c) * s;
+  nd.r = drcp(ds);
   Seg o;
-  o.F.a = A.F.a;
-  o.F.b = fma(A.F.c, nd.p1, A.F.b);
+  o.F.a = A.F.a * ds;
+  o.F.b = fma(A.F.c, nd.p1, A.F.b * ds);
   o.F.c = A.F.c * nd.p2;
-  o.F.d = fma(-A.F.c, nd.p0, A.F.d);
+  o.F.d = fma(-A.F.c, nd.p0, A.F.d * ds);
   o.L.a = B.L.a * nd.q1;
-  o.L.b = fma(B.L.a, nd.q2, B.L.b);
-  o.L.c = B.L.c;
-  o.L.d = fma(-B.L.a, nd.q0, B.L.d);
+  o.L.b = fma(B.L.a, nd.q2, B.L.b * ds);
+  o.L.c = B.L.c * ds;
+  o.L.d = fma(-B.L.a, nd.q0, B.L.d * ds);
   out = o;
+}
+
+// Downsweep step of one node: (xf, xl) of the merged segment -> x[l1], x[f2].
+__device__ __forceinline__ void split_node(const Node& nd, double xf, double xl, double& xl1,
+                                           double& xf2) {
+  xl1 = fma(nd.p2, xl, fma(nd.p1, xf, nd.p0)) * nd.r;
+  xf2 = fma(nd.q2, xl, fma(nd.q1, xf, nd.q0)) * nd.r;
 }
 
 __device__ __forceinline__ Seg shfl_down_seg(const Seg& s, int delta) {
@@ -145,12 +169,18 @@ __device__ __forceinline__ Seg block_reduce(const Acc& r, int m_rt, bool& bad) {
   return S;
 }
 
-// Stage 1 for Stage 3's benefit: as block_reduce, but the forward sweep's
-// reciprocals and c' are kept in the row storage (b(j) <- 1/den_j,
-// c(j) <- c'_j for interior j < L; c(L) keeps c_{e-1}) so that
-// block_interior_kept needs no reciprocal on its dependency chain.
-template <int M, class Acc>
-__device__ __forceinline__ Seg block_reduce_keep(Acc& r, bool& bad) {
+// Stage 1 with a short dependency chain (compile-time m, rows in registers).
+// The pivots of the interior sweep are ratios of continuants,
+//   den_j = q_j / q_{j-1},  q_0 = 1, q_1 = b_1,
+//   q_j = b_j q_{j-1} - (a_j c_{j-1}) q_{j-2},
+// an FMA-only recurrence; the reciprocals inv_j = q_{j-1} / q_j are then
+// independent of each other, and the y'/g' sweeps become FMA+MUL chains.
+// A zero or non-finite continuant (a zero pivot, or over/underflow for
+// extreme inputs) drops the block to the classic sweep.
+// KEEP (Stage 3): b(j) <- inv_j and c(j) <- c'_j for interior j < L, c(L)
+// unchanged, for block_interior_kept.
+template <int M, bool KEEP, class Acc>
+__device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
   static_assert(M > 0, "compile-time m only");
   Seg S;
   if constexpr (M == 2) {
@@ -159,31 +189,52 @@ __device__ __forceinline__ Seg block_reduce_keep(Acc& r, bool& bad) {
     return S;
   } else {
     constexpr int L = M - 2;
-    double den = r.b(1);
-    bad |= (den == 0.0);
-    double inv = drcp(den);
-    double cp = (L > 1) ? r.c(1) * inv : 0.0;
-    double yp = r.d(1) * inv;
-    double gp = r.a(1) * inv;
+    double q[L + 1], inv[L + 1];
+    q[0] = 1.0;
+    q[1] = r.b(1);
+    bool ok = q[1] != 0.0;
+#pragma unroll
+    for (int j = 2; j <= L; ++j) {
+      q[j] = fma(r.b(j), q[j - 1], -(r.a(j) * r.c(j - 1)) * q[j - 2]);
+      ok &= (q[j] != 0.0);
+    }
+    ok &= isfinite(q[L]) && (fabs(q[L]) > 1e-280);
+    if (ok) {
+#pragma unroll
+      for (int j = 1; j <= L; ++j) inv[j] = q[j - 1] * drcp(q[j]);
+    } else {  // classic sweep (rare)
+      double cprev = 0.0;
+#pragma unroll
+      for (int j = 1; j <= L; ++j) {
+        const double den = (j == 1) ? r.b(1) : fma(-r.a(j), cprev, r.b(j));
+        bad |= (den == 0.0);
+        inv[j] = drcp(den);
+        cprev = r.c(j) * inv[j];
+      }
+    }
+    double cp = (L > 1) ? r.c(1) * inv[1] : 0.0;
+    double yp = r.d(1) * inv[1];
+    double gp = r.a(1) * inv[1];
     double P = 1.0, Y1 = yp, G1 = gp;
-    r.B[1] = inv;
-    if (L > 1) r.C[1] = cp;
+    if constexpr (KEEP) {
+      r.B[1] = inv[1];
+      if (L > 1) r.C[1] = cp;
+    }
 #pragma unroll
     for (int j = 2; j <= L; ++j) {
       const double aj = r.a(j);
-      den = fma(-aj, cp, r.b(j));
-      bad |= (den == 0.0);
-      inv = drcp(den);
       P = -P * cp;
-      yp = fma(-aj, yp, r.d(j)) * inv;
-      gp = -aj * gp * inv;
-      cp = (j < L) ? r.c(j) * inv : 0.0;
+      yp = fma(-aj, yp, r.d(j)) * inv[j];
+      gp = -aj * gp * inv[j];
+      cp = (j < L) ? r.c(j) * inv[j] : 0.0;
       Y1 = fma(P, yp, Y1);
       G1 = fma(P, gp, G1);
-      r.B[j] = inv;
-      if (j < L) r.C[j] = cp;
+      if constexpr (KEEP) {
+        r.B[j] = inv[j];
+        if (j < L) r.C[j] = cp;
+      }
     }
-    const double hL = r.c(L) * inv;
+    const double hL = r.c(L) * inv[L];
     const double H1 = P * hL;
     const double as = r.a(0), bs = r.b(0), cs = r.c(0), ds = r.d(0);
     const double ae = r.a(M - 1), be = r.b(M - 1), ce = r.c(M - 1), de = r.d(M - 1);
@@ -193,7 +244,7 @@ __device__ __forceinline__ Seg block_reduce_keep(Acc& r, bool& bad) {
   }
 }
 
-// Stage 3 after block_reduce_keep: forward substitution with the stored
+// Stage 3 after block_reduce_fast<M, true>: forward substitution with the stored
 // reciprocals (an FMA + MUL chain per row), then back-substitution; x is
 // written over b(j).
 template <int M, class Acc>

@@ -283,9 +283,8 @@ __device__ __forceinline__ void down_level(const Node* nodes, int stride, int la
   const bool left = lane < active && (lane & (2 * stride - 1)) == 0 && right_nonempty;
   double sf = 0.0, sl = 0.0;
   if (left) {
-    const Node nd = nodes[lane / (2 * stride)];
-    const double xl1 = fma(nd.p2, xl, fma(nd.p1, xf, nd.p0));
-    const double xf2 = fma(nd.q2, xl, fma(nd.q1, xf, nd.q0));
+    double xl1, xf2;
+    split_node(nodes[lane / (2 * stride)], xf, xl, xl1, xf2);
     sf = xf2;
     sl = xl;
     xl = xl1;
@@ -422,7 +421,7 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
         __syncthreads();  // stage s fully consumed -> refill it
         if (tid == 0 && k + S < nlocal) issue(s, tile_of(k + S));
       }
-      seg = block_reduce<M>(regs, m, bad);
+      seg = block_reduce_fast<M, false>(regs, bad);
     } else {
       sacc.fixup(r0, m, ctx);
       seg = block_reduce<0>(sacc, m, bad);
@@ -540,12 +539,22 @@ __host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages) {
   return (bytes + 127) / 128 * 128;
 }
 
+#ifndef PM_SOLVE_MINB
+#define PM_SOLVE_MINB 1
+#endif
+#ifndef PM_REDUCE_MINB
+#define PM_REDUCE_MINB 1
+#endif
 template <int M, int MODE>
-__global__ void __launch_bounds__(128) warp_tile_kernel(TileArgs args) {
+__global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : PM_SOLVE_MINB))
+    warp_tile_kernel(TileArgs args) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int m = (M > 0) ? M : args.m;
   const int T = 32 * m;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // warp index through a lane-0 broadcast: provably warp-uniform, so the
+  // tile loop below is convergent and its shuffles compile to plain SHFL
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int S = args.stages;
   const int r0 = lane * m;
   const size_t per_warp = warp_smem_bytes(MODE, m, S);
@@ -627,10 +636,7 @@ __global__ void __launch_bounds__(128) warp_tile_kernel(TileArgs args) {
       regs.load(sa, sb, sc, sd, r0, ctx);
       __syncwarp();
       if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));  // early release
-      if constexpr (MODE == kModeReduce)
-        seg = block_reduce<M>(regs, m, bad);
-      else
-        seg = block_reduce_keep<M>(regs, bad);
+      seg = block_reduce_fast<M, MODE != kModeReduce>(regs, bad);
     } else {
       sacc.fixup(r0, m, ctx);
       seg = block_reduce<0>(sacc, m, bad);
@@ -760,9 +766,8 @@ __global__ void dist_chain_kernel(const double* __restrict__ iface, int world, i
   double xl = fma(acc.F.b, acc.L.d, -acc.L.a * acc.F.d) * inv;        // x_last of rank k
   double xf = x0;
   for (int k = world - 1; k >= 1 && k >= rank; --k) {
-    const Node nd = chain_nodes[k];
-    const double xl_prev = fma(nd.p2, xl, fma(nd.p1, x0, nd.p0));
-    const double xf_k = fma(nd.q2, xl, fma(nd.q1, x0, nd.q0));
+    double xl_prev, xf_k;
+    split_node(chain_nodes[k], x0, xl, xl_prev, xf_k);
     if (k == rank) {
       xf = xf_k;
       break;

@@ -38,7 +38,7 @@ class DistributedSolver:
     """Collective row-sharded solve over an initialised torch.distributed group
     (backend nccl on GPUs; every rank calls `solve`)."""
 
-    def __init__(self, solver, group=None):
+    def __init__(self, solver, group=None, device=None):
         import torch
         import torch.distributed as dist
 
@@ -47,7 +47,7 @@ class DistributedSolver:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        dev = torch.device("cuda", solver.device)
+        dev = device if device is not None else torch.device("cuda", solver.device)
         self.iface = torch.zeros(8, dtype=torch.float64, device=dev)
         self.iface_all = torch.zeros(8 * self.world, dtype=torch.float64, device=dev)
 

@@ -24,6 +24,8 @@ PM_OPT_MAX_CTAS = 4
 PM_OPT_TIMINGS = 5
 PM_OPT_KERNEL_TIMES = 6
 PM_OPT_WARP_TILES = 7
+PM_OPT_SOLVE_STAGES = 8
+PM_OPT_WARPS_PER_CTA = 9
 PM_MAX_M = 128
 
 

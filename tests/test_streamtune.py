@@ -1,0 +1,315 @@
+"""CPU tests of the streamtune C++ API (through include/streamtune_c.h).
+
+Vectors are the reference spec's examples and acceptance criteria
+ and the paper's tables; the timing identities are
+also pinned bit-for-bit to the reference's own header compiled into
+oracle/_ref/libstreamtune_ref.so (oracle/ref_shim.cpp).
+"""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2501_05938_b200 import errors
+from paper_2501_05938_b200 import streamtune as st
+from paper_2501_05938_b200.solver import StageTimings
+
+PAPER = st.ModelBundle.paper()
+TAU = 0.004448
+
+TABLE1 = [  # size, t1_comp, t1_d2h, t3_h2d, t3_comp, sum, gomez-luna
+    (4e3, 0.221312, 0.014848, 0.006592, 0.030688, 0.273440, 7.8),
+    (4e4, 0.216544, 0.057312, 0.015456, 0.038112, 0.327424, 8.6),
+    (4e5, 0.393184, 0.402944, 0.102784, 0.205408, 1.104320, 15.8),
+    (4e6, 1.993980, 3.897410, 0.975392, 2.130500, 8.997282, 45.0),
+    (4e7, 17.451500, 38.836800, 9.606720, 20.981600, 86.876620, 139.8),
+]
+TABLE2 = [  # n, t_str, t_non_str, sum, overhead, benefit
+    (2, 7.999136, 8.817440, 2.433568, 0.398480, 0.818304),
+    (4, 7.533248, 8.817440, 2.433568, 0.540984, 1.284192),
+    (8, 7.401472, 8.817440, 2.433568, 0.713404, 1.415968),
+    (16, 7.445952, 8.817440, 2.433568, 0.909982, 1.371488),
+    (32, 7.599968, 8.817440, 2.433568, 1.140047, 1.217472),
+]
+TABLE4 = [(1e3, 1, 1), (4e3, 1, 1), (5e3, 1, 1), (8e3, 1, 1), (1e4, 1, 1), (4e4, 1, 1), (5e4, 1, 1),
+          (8e4, 1, 1), (1e5, 1, 2), (4e5, 4, 4), (5e5, 8, 4), (8e5, 8, 8), (1e6, 8, 8), (2.5e6, 16, 16),
+          (4e6, 32, 32), (5e6, 32, 32), (7.5e6, 32, 32), (8e6, 32, 32), (1e7, 32, 32), (2.5e7, 32, 32),
+          (4e7, 32, 32), (5e7, 32, 32), (7.5e7, 32, 32), (8e7, 32, 32), (1e8, 32, 32)]
+
+
+def _t(**kw):
+    t = StageTimings(slae_size=kw.pop("slae_size", 1000))
+    for k, v in kw.items():
+        setattr(t, k, v)
+    return t
+
+
+# ---- timing_model ---------------------------------------------------
+def test_total_and_overlap_examples():
+    assert st.total_unstreamed(_t()) == 0.0
+    assert st.total_unstreamed(_t(t1_h2d=1, t1_comp=1, t1_d2h=1, t2_comp=1, t3_h2d=1, t3_comp=1,
+                                  t3_d2h=1)) == 7.0
+    for size, c1, d1, h3, c3, s, _ in TABLE1:
+        t = _t(slae_size=int(size), t1_comp=c1, t1_d2h=d1, t3_h2d=h3, t3_comp=c3)
+        assert abs(st.overlap_sum(t) - s) < 1e-9
+
+
+def test_table2_consistent_fixture():
+    # back-solve a StageTimings consistent with Table 2 (sum 2.433568, T 8.817440)
+    t = _t(slae_size=1_000_000, t1_comp=0.6, t1_d2h=0.9, t3_h2d=0.233568, t3_comp=0.7, t1_h2d=4.85,
+           t2_comp=0.32, t3_d2h=8.817440 - 4.85 - 0.32 - 2.433568)
+    assert abs(st.total_unstreamed(t) - 8.817440) < 1e-12
+    assert abs(st.overlap_sum(t) - 2.433568) < 1e-12
+
+
+def test_table2_identities():
+    best = max(TABLE2, key=lambda r: r[5])
+    assert best[0] == 8
+    for n, tstr, tnon, s, ovh, ben in TABLE2:
+        o = st.overhead_from_measurement(tstr, tnon, n, s)
+        assert abs(o - ovh) < 1e-6
+        assert abs(st.overlap_benefit(n, s, o) - ben) < 1e-6
+        assert abs(st.overlap_benefit(n, s, o) - (tnon - tstr)) < 1e-12
+    assert st.overhead_from_measurement(3.3, 3.3, 1, 9.0) == 0.0
+    assert st.overlap_benefit(1, 5.0, 0.0) == 0.0
+
+
+def test_streamed_lower_bound():
+    t = _t(t1_h2d=4, t1_comp=2, t1_d2h=1, t2_comp=0.5, t3_h2d=0.25, t3_comp=1, t3_d2h=3)
+    assert st.streamed_lower_bound(t, 1, 0.0) == st.total_unstreamed(t)
+    vals = [st.streamed_lower_bound(t, n, 0.0) for n in (1, 2, 4, 8, 16, 32)]
+    assert all(x > y for x, y in zip(vals, vals[1:]))
+    assert vals[-1] > 4 + 0.5 + 3
+
+
+def test_stream_count_validation():
+    assert [n for n in range(0, 70) if st.stream_count_is_valid(n)] == [1, 2, 4, 8, 16, 32]
+    for bad in (0, 3, 64, -2):
+        with pytest.raises(errors.InvalidStreamCountError):
+            st.overlap_benefit(bad, 1.0, 0.0)
+
+
+def test_stage_timings_validation():
+    st.validate_stage_timings(_t(t1_h2d=1.0))
+    with pytest.raises(errors.NegativeDurationError):
+        st.validate_stage_timings(_t(t1_comp=-1.0))
+    with pytest.raises(errors.ValidationError):
+        st.validate_stage_timings(_t(t2_comp=float("nan")))
+    with pytest.raises(errors.ValidationError):
+        st.validate_stage_timings(_t(slae_size=0))
+
+
+def test_timing_model_bit_identical_to_reference_header():
+    """Pins include/streamtune/timing_model.hpp to the reference's header."""
+    R = oracle.ref_lib()
+    rng = np.random.default_rng(7)
+    D = C.POINTER(C.c_double)
+    for _ in range(2000):
+        v = rng.uniform(0, 100, 7) * 10.0 ** rng.integers(-4, 3, 7)
+        arr = (C.c_double * 7)(*v)
+        t = _t(slae_size=1, t1_h2d=v[0], t1_comp=v[1], t1_d2h=v[2], t2_comp=v[3], t3_h2d=v[4],
+               t3_comp=v[5], t3_d2h=v[6])
+        assert st.total_unstreamed(t) == R.ref_total_unstreamed(arr)
+        assert st.overlap_sum(t) == R.ref_overlap_sum(arr)
+        n = int(2 ** rng.integers(0, 6))
+        ovh = float(rng.uniform(-1, 3))
+        out = C.c_double()
+        assert R.ref_streamed_lower_bound(arr, n, ovh, C.byref(out)) == 0
+        assert st.streamed_lower_bound(t, n, ovh) == out.value
+        ts, tn, s = float(rng.uniform(0, 50)), float(rng.uniform(0, 50)), float(rng.uniform(0, 10))
+        assert R.ref_overhead_from_measurement(ts, tn, n, s, C.byref(out)) == 0
+        assert st.overhead_from_measurement(ts, tn, n, s) == out.value
+        assert R.ref_overlap_benefit(n, s, ovh, C.byref(out)) == 0
+        assert st.overlap_benefit(n, s, ovh) == out.value
+    for n in range(-3, 70):
+        assert bool(R.ref_stream_count_is_valid(n)) == st.stream_count_is_valid(n)
+    # validation behaviour
+    err = C.create_string_buffer(256)
+    neg = (C.c_double * 7)(1, -1, 1, 1, 1, 1, 1)
+    assert R.ref_validate_stage_timings(neg, 5, err, 256) == 3
+    with pytest.raises(errors.NegativeDurationError):
+        st.validate_stage_timings(_t(slae_size=5, t1_h2d=1, t1_comp=-1))
+
+
+# ---- predictor ---------------------------------------------------------
+def test_predict_examples():
+    assert abs(st.predict_sum(PAPER, 1) - 0.1470666889) < 1e-9
+    assert abs(st.predict_sum(PAPER, 10**6) - 2.3360662148) < 1e-9
+    assert abs(st.predict_sum(PAPER, 10**7) - 22.0370816490) < 1e-9
+    assert abs(st.predict_overhead(PAPER, 10**6, 1) - 0.1640461720) < 1e-9
+    assert abs(st.predict_overhead(PAPER, 10**7, 32) - 3.1199) < 1e-4
+    # threshold inclusive on the small side
+    assert st.recommend(PAPER, 10**6).model_used == "small"
+    assert st.recommend(PAPER, 10**6 + 1).model_used == "big"
+
+
+def test_recommend_table4():
+    """SPEC criterion 1.  24/25 reproduce; 8e4 gives 2, not Table 4's 1
+    (benefit(2) = +0.0227 with the printed coefficients)."""
+    mismatches = []
+    for size, _, pre in TABLE4:
+        got = st.recommend(PAPER, int(size)).chosen
+        if got != pre:
+            mismatches.append((int(size), got, pre))
+    assert mismatches == [(80_000, 2, 1)]
+    r = st.recommend(PAPER, 80_000)
+    assert abs(r.benefits[0] - 0.022744) < 1e-5
+    assert st.recommend(PAPER, 10**5).chosen == 2
+    assert st.recommend(PAPER, 5 * 10**5).chosen == 4
+    r = st.recommend(PAPER, 10**6)
+    assert r.chosen == 8
+    assert np.allclose(r.benefits, [0.823, 1.226, 1.337, 1.302, 1.194], atol=2e-3)
+
+
+def test_recommend_fp32_and_gomez_luna():
+    assert st.recommend_fp32(PAPER, 10**6) == 4
+    assert st.recommend_fp32(PAPER, 4 * 10**5) == 2
+    assert st.recommend_fp32(PAPER, 10**3) == 1
+    for size, *_, s, gl in TABLE1:
+        assert abs(st.gomez_luna_optimum(s, TAU) - gl) <= 0.05
+        assert abs(st.gomez_luna_optimum(s, TAU) ** 2 * TAU - s) < 1e-12 * max(1, s)
+    assert st.gomez_luna_optimum(0.0, TAU) == 0.0
+    with pytest.raises(errors.NonpositiveTauError):
+        st.gomez_luna_optimum(1.0, 0.0)
+
+
+def test_recommend_invariants():
+    rng = np.random.default_rng(3)
+    for _ in range(200):
+        n = int(10 ** rng.uniform(3, 8))
+        base = st.recommend(PAPER, n)
+        k = float(rng.uniform(0.1, 10))
+        sc = st.ModelBundle(PAPER.sum_a * k, PAPER.sum_b * k, PAPER.small_a * k, PAPER.small_b * k,
+                            PAPER.small_c * k, PAPER.big_a * k, PAPER.big_b * k, PAPER.big_c * k)
+        assert st.recommend(sc, n).chosen == base.chosen
+        infl = st.ModelBundle(**{**PAPER.__dict__, "small_c": PAPER.small_c + 0.5,
+                                 "big_c": PAPER.big_c + 0.5})
+        assert sum(b > 0 for b in st.recommend(infl, n).benefits) <= sum(b > 0 for b in base.benefits)
+
+
+def test_recommend_through_solver_abi():
+    from paper_2501_05938_b200 import recommend_streams
+
+    assert [recommend_streams(int(s)) for s, _, _ in TABLE4][:9] == [1] * 7 + [2, 2]
+    assert recommend_streams(10**6, PAPER.to_c()) == 8
+
+
+# ---- regression ------------------------------------------------------------
+def test_split_properties():
+    tr, te = st.train_test_split(8, 0.75, True, 42)
+    assert len(tr) == 6 and len(te) == 2 and sorted(tr + te) == list(range(8))
+    assert st.train_test_split(8, 0.75, True, 42) == (tr, te)
+    assert st.train_test_split(8, 0.75, False, 42) == (list(range(6)), [6, 7])
+    assert st.train_test_split(30, 0.75, True, 1) != st.train_test_split(30, 0.75, True, 2)
+    with pytest.raises(errors.TooFewObservationsError):
+        st.train_test_split(3, 0.75, True, 42)
+
+
+def test_least_squares_examples():
+    assert np.allclose(st.fit_least_squares([[0, 1], [1, 1], [2, 1]], [1, 3, 5]), [2, 1], atol=1e-12)
+    with pytest.raises(errors.RankDeficiencyError):
+        st.fit_least_squares([[1, 1], [2, 2], [3, 3]], [1, 2, 3])
+    xs = np.geomspace(1e3, 1e8, 8)
+    beta = st.fit_least_squares(np.stack([xs, np.ones(8)], 1), 0.0000021890017149 * xs + 0.1470644998564126)
+    assert abs(beta[0] / 0.0000021890017149 - 1) < 1e-9 and abs(beta[1] / 0.1470644998564126 - 1) < 1e-9
+
+
+def test_coefficient_recovery_property():
+    """SPEC criterion 4: 100 random triples per model form, noiseless data."""
+    rng = np.random.default_rng(11)
+    sizes = [int(10 ** e) for e in np.linspace(3, 8, 6)]
+    streams = [2, 4, 8, 16, 32]
+    rows = [(s, n) for s in sizes for n in streams]
+    S = [r[0] for r in rows]
+    N = [r[1] for r in rows]
+    for _ in range(100):
+        a, b = rng.uniform(1e-8, 1e-5), rng.uniform(0.01, 1)
+        rep = st.fit_model("sum", sizes + [3000, 70000], [a * s + b for s in sizes + [3000, 70000]])
+        assert np.allclose(rep.coefficients, [a, b], rtol=1e-9) and abs(rep.train["r_squared"] - 1) < 1e-12
+        a, b, c = rng.uniform(1e-9, 1e-6), rng.uniform(0.1, 1), rng.uniform(-0.5, 0.5)
+        y = [a * s + b * math.log10(n) + c for s, n in rows]
+        rep = st.fit_model("small", S, y, N)
+        assert np.allclose(rep.coefficients, [a, b, c], rtol=1e-9, atol=1e-12)
+        a, b, c = rng.uniform(1e-10, 1e-7), rng.uniform(0.01, 0.2), rng.uniform(0.1, 1)
+        y = [(a * s + b) * (4 / 3) * math.log2(n) + c for s, n in rows]
+        rep = st.fit_model("big", S, y, N)
+        assert np.allclose(rep.coefficients, [a, b, c], rtol=1e-9, atol=1e-12)
+        assert abs(rep.train["rmse"] ** 2 - rep.train["mse"]) <= 1e-12 * max(rep.train["mse"], 1e-300)
+
+
+def test_overhead_fits_degenerate_designs():
+    # only n = 1 rows: both log features vanish -> rank deficiency
+    with pytest.raises(errors.RankDeficiencyError):
+        st.fit_model("big", [1e6, 1e7, 1e8, 2e7, 3e6, 5e6], [1] * 6, [1] * 6)
+    with pytest.raises(errors.RankDeficiencyError):
+        st.fit_model("small", [1e4] * 6, [1] * 6, [1] * 6)
+
+
+def test_metrics_examples():
+    m = st.metrics([1, 2, 3], [1, 2, 3])
+    assert m["r_squared"] == 1 and m["mse"] == 0 and m["rmse"] == 0
+    assert st.metrics([2, 2, 2], [1, 2, 3])["r_squared"] == 0.0
+    m = st.metrics([0, 1], [1, 0])
+    assert m["mse"] == 1 and m["rmse"] == 1
+    with pytest.raises(errors.ZeroVarianceError):
+        st.metrics([1, 2], [3, 3])
+
+
+# ---- dataset ---------------------------------------------------------------
+STAGE_HDR = "slae_size,t1_h2d,t1_comp,t1_d2h,t2_comp,t3_h2d,t3_comp,t3_d2h\n"
+RUNS_HDR = "slae_size,num_streams,t_str\n"
+
+
+def _stage_csv_table2():
+    # consistent StageTimings for 1e6 (sum 2.433568, T_non_str 8.817440)
+    return STAGE_HDR + "1000000,4.85,0.6,0.9,0.32,0.233568,0.7,1.213872\n"
+
+
+def test_loaders_and_errors():
+    rows = st.load_stage_timings(STAGE_HDR + "1000,1,2,3,4,5,6,7\n")
+    assert len(rows) == 1 and rows[0].t3_d2h == 7.0
+    with pytest.raises(errors.DuplicateSizeError):
+        st.load_stage_timings(STAGE_HDR + "10,1,1,1,1,1,1,1\n10,1,1,1,1,1,1,1\n")
+    with pytest.raises(errors.NegativeDurationError):
+        st.load_stage_timings(STAGE_HDR + "10,1,-1.0,1,1,1,1,1\n")
+    with pytest.raises(errors.MalformedRowError):
+        st.load_stage_timings(STAGE_HDR + "10,1,x,1,1,1,1,1\n")
+    with pytest.raises(errors.InvalidStreamCountError):
+        st.load_streamed_runs(RUNS_HDR + "1000,3,1.0\n")
+    assert st.load_streamed_runs(RUNS_HDR) == []
+    runs = RUNS_HDR + "".join(f"1000000,{n},{t}\n" for n, t, *_ in TABLE2)
+    assert len(st.load_streamed_runs(runs)) == 5
+
+
+def test_derive_overhead_rows_table2():
+    runs = RUNS_HDR + "1000000,1,8.8\n" + "".join(f"1000000,{n},{t}\n" for n, t, *_ in TABLE2)
+    rows = st.derive_overhead_rows(_stage_csv_table2(), runs)
+    assert [r[1] for r in rows] == [2, 4, 8, 16, 32]  # n = 1 skipped
+    assert np.allclose([r[2] for r in rows], [r[4] for r in TABLE2], atol=1e-6)
+    with pytest.raises(errors.MissingStageTimingsError):
+        st.derive_overhead_rows(_stage_csv_table2(), RUNS_HDR + "5,2,1.0\n")
+
+
+def test_fit_bundle_recovers_paper_coefficients():
+    """cmd_fit on noiseless data generated from the paper's models."""
+    sizes = [int(k * 10 ** i) for i in range(3, 8) for k in (1, 2.5, 4, 5, 7.5, 8)]
+    stage = STAGE_HDR
+    runs = RUNS_HDR
+    for s in sizes:
+        ssum = st.predict_sum(PAPER, s)
+        t1h, t2, t3d = 1.0, 0.2, 0.5
+        q = ssum / 4
+        stage += f"{s},{t1h},{q},{q},{t2},{q},{q},{t3d}\n"
+        tnon = t1h + t2 + t3d + ssum
+        for n in (1, 2, 4, 8, 16, 32):
+            ovh = st.predict_overhead(PAPER, s, n) if n > 1 else 0.0
+            tstr = tnon - (n - 1) / n * ssum + ovh
+            runs += f"{s},{n},{tstr!r}\n"
+    b, met = st.fit_bundle(stage, runs)
+    for k in ("sum_a", "sum_b", "small_a", "small_b", "small_c", "big_a", "big_b", "big_c"):
+        assert abs(getattr(b, k) / getattr(PAPER, k) - 1) < 1e-6, k
+    assert met["sum"]["train"]["r_squared"] > 0.999999
+    with pytest.raises(errors.TooFewObservationsError):
+        st.fit_bundle(stage, RUNS_HDR + "1000,1,1.0\n")
