@@ -269,6 +269,10 @@ def main():
         return (sum(v) / len(v)) if v else float("nan")
 
     t_solve, t_reduce = avg(1), avg(0)
+    per_kernel = {}
+    for (md, lv, t) in ktimes:
+        per_kernel.setdefault(f"{['reduce', 'solve', 'root', 'up_solve'][md]}_L{lv}", []).append(t)
+    per_kernel = {k: round(sum(v) / len(v), 5) for k, v in sorted(per_kernel.items())}
     t_kern_total = sum(t for (_, _, t) in ktimes) / args.steps
     peak, peak_src = peaks()
     ach_solve = BYTES_SOLVE * n_loc / (t_solve / 1e3) / 1e9
@@ -338,7 +342,8 @@ def main():
                          "whole_solve": {"achieved": BYTES_TOTAL * n_loc / (ms_per_step / 1e3) / 1e9,
                                          "frac": BYTES_TOTAL * n_loc / (ms_per_step / 1e3) / 1e9 / peak,
                                          "bytes_per_unknown": BYTES_TOTAL,
-                                         "kernel_ms_sum": t_kern_total}},
+                                         "kernel_ms_sum": t_kern_total},
+                         "kernels_ms": per_kernel},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,

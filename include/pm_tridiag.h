@@ -87,8 +87,13 @@ typedef struct pm_model_bundle {
 #define PM_OPT_WARP_TILES 7    /* 1 (default): level 0 uses warp-owned tiles of
                                   32*m rows; 0: CTA tiles (P*m rows, P <= 128)     */
 #define PM_OPT_SOLVE_STAGES 8  /* ring depth of the level-0 Stage-3 kernel
-                                  (0 = PM_OPT_STAGES)                              */
+                                  (default 1; 0 = PM_OPT_STAGES)                   */
 #define PM_OPT_WARPS_PER_CTA 9 /* warps per CTA of the warp-tile kernels (1..8)    */
+#define PM_OPT_CHAIN 10        /* 1: level-0 warps chain contiguous tile chunks, so
+                                  level 1 is a single ROOT tile (default 0)        */
+#define PM_OPT_UPPER_M 11      /* rows per thread of the warp-tile upper levels
+                                  (default 0 = CTA tiles with m = 8)               */
+#define PM_OPT_ROOT_M 12       /* ROOT tile = 128 * root_m rows (default 8)        */
 
 int pm_create(pm_handle_t* out, int device);
 int pm_destroy(pm_handle_t h);

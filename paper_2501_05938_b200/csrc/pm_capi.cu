@@ -72,7 +72,7 @@ struct pm_handle_s {
   int max_ctas = 0;
   int timings = 0;
   int warp_tiles = 1;
-  int solve_stages = 0;   // 0 = same as `stages`
+  int solve_stages = 1;   // level-0 Stage 3 ring depth (0 = same as `stages`)
   int warps_per_cta = 4;
   // device scratch for upper levels (+ dist boundary values)
   double* scratch = nullptr;
@@ -90,6 +90,14 @@ struct pm_handle_s {
   int last_streams = 0;
   int launches = 0;
   std::vector<Level> levels;
+  // chain mode (level 0 warp tiles): per part (stream chunk) chunk counts
+  bool chain = false;
+  int nparts = 1;
+  int opt_chain = 0;
+  int upper_m = 0;   // warp-tile m of the upper levels (0: CTA tiles, m = 8)
+  int root_m = 8;    // ROOT tile: 128 * root_m rows
+  std::vector<int64_t> part_chunks, part_base;
+  void* chain_nodes = nullptr;
   // per-launch CUDA-event timing (PM_OPT_KERNEL_TIMES)
   int ktimes = 0;
   std::vector<cudaEvent_t> kev;
@@ -134,11 +142,31 @@ int pick_stages(int want, int P, int m) {
   return S;
 }
 
+// Warp-tile configuration of a level: ring depth and as many warps per CTA
+// (<= PM_OPT_WARPS_PER_CTA) as the shared memory allows.
+void set_warp_tiles(pm_handle_t h, Level& L) {
+  int S = std::max(1, std::min(std::max(h->stages, h->solve_stages), 4));
+  int W = 0;
+  while (S >= 1) {
+    W = (int)std::min<size_t>(h->warps_per_cta,
+                              kSmemLimit / pm::warp_smem_bytes(pm::kModeReduce, L.m, S));
+    W = (int)std::min<size_t>(W, kSmemLimit / pm::warp_smem_bytes(pm::kModeSolve, L.m, 1));
+    if (W >= 1) break;
+    --S;
+  }
+  if (W >= 1) {
+    L.P = 32;
+    L.stages = S;
+    L.warps_per_cta = W;
+  }
+}
+
 // Builds h->levels for a level-0 system; allocates scratch for levels >= 1.
 // ragged0: the caller's last tile must not be padded (row-sharded ranks that
 // are not the last one); then m must divide n and upper levels use m = 2.
 int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b, const double* c,
-               const double* d, double* x, bool ragged0, size_t extra_doubles) {
+               const double* d, double* x, bool ragged0, size_t extra_doubles,
+               bool allow_chain = true, int nparts = 1) {
   std::vector<Level> lv;
   Level L0;
   L0.n = n;
@@ -146,22 +174,9 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   L0.a = a; L0.b = b; L0.c = c; L0.d = d; L0.x = x;
   L0.pad_mode = ragged0 ? 0 : 1;
   L0.bulk = aligned16(a) && aligned16(b) && aligned16(c) && aligned16(d) && aligned16(x);
-  if (L0.bulk && h->warp_tiles) {
-    // warp tiles: as many warps per CTA (<= 4) as the shared memory allows
-    int S = std::max(1, std::min(std::max(h->stages, h->solve_stages), 4));
-    int W = 0;
-    while (S >= 1) {
-      W = (int)std::min<size_t>(h->warps_per_cta,
-                                kSmemLimit / pm::warp_smem_bytes(pm::kModeSolve, m, S));
-      if (W >= 1) break;
-      --S;
-    }
-    if (W >= 1) {
-      L0.P = 32;
-      L0.stages = S;
-      L0.warps_per_cta = W;
-    }
-  }
+  // a system that fits one CTA tile is solved by a single ROOT launch
+  const bool one_tile = n <= (int64_t)choose_P(m) * m;
+  if (L0.bulk && h->warp_tiles && !one_tile) set_warp_tiles(h, L0);
   if (L0.warps_per_cta == 0) {
     L0.P = choose_P(m);
     L0.stages = pick_stages(h->stages, L0.P, m);
@@ -171,16 +186,67 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   L0.T = (int64_t)L0.P * m;
   L0.ntiles = (n + L0.T - 1) / L0.T;
   lv.push_back(L0);
+  // Chain mode (single system / batch on warp tiles): level 0's tiles form C
+  // contiguous chunks (C = the Stage-3 kernel's resident warps); each warp
+  // chains its chunk's tile segments, so level 1 has 2C rows and is solved by
+  // one ROOT launch.  Otherwise every upper level is a CTA-tile REDUCE/SOLVE
+  // launch pair and the top a ROOT launch (m_up = 8, or 2 for the ragged
+  // levels of a row-sharded rank).
+  h->chain = h->opt_chain && allow_chain && !ragged0 && L0.warps_per_cta > 0 && L0.ntiles > 1;
+  nparts = (int)std::max<int64_t>(1, std::min<int64_t>(nparts, L0.ntiles));
+  h->nparts = nparts;
+  h->part_chunks.clear();
+  h->part_base.clear();
+  if (h->chain) {
+    const int ctas = pm::warp_kernel_ctas_per_sm(pm::kModeSolve, m, std::max(1, std::min(h->solve_stages > 0 ? h->solve_stages : L0.stages, L0.stages)),
+                                                 L0.warps_per_cta, true);
+    int64_t C = (int64_t)std::max(1, ctas) * L0.warps_per_cta * h->sm_count;
+    C = std::min<int64_t>(C, 8192);
+    int64_t total = 0;
+    for (int k = 0; k < nparts; ++k) {
+      const int64_t t0 = L0.ntiles * k / nparts, t1 = L0.ntiles * (k + 1) / nparts;
+      int64_t ck = std::max<int64_t>(1, C * (t1 - t0) / L0.ntiles);
+      ck = std::min<int64_t>(ck, t1 - t0);
+      if (t1 == t0) ck = 0;
+      h->part_base.push_back(total);
+      h->part_chunks.push_back(ck);
+      total += ck;
+    }
+    Level U;
+    U.n = 2 * total;
+    U.m = (int)std::max<int64_t>(8, (U.n + 127) / 128);
+    U.P = 128;
+    U.T = (int64_t)U.P * U.m;
+    U.ntiles = 1;
+    U.pad_mode = 1;
+    U.bulk = true;
+    U.stages = 1;
+    if (U.m > PM_MAX_M) return fail(h, PM_ERR_RUNTIME, "chain root too large");
+    lv.push_back(U);
+  }
+  // Upper levels: warp tiles of 32*upper_m rows while the level exceeds one
+  // ROOT tile (128*root_m rows), then the ROOT; ragged ranks use CTA tiles
+  // with m = 2.
+  const int m_up = ragged0 ? 2 : 8;
   while (lv.back().ntiles > 1) {
     const Level& prev = lv.back();
     Level U;
     U.n = 2 * prev.ntiles;
-    U.m = ragged0 ? 2 : 8;
+    U.pad_mode = ragged0 ? 0 : 1;
+    U.bulk = true;
     U.P = 128;
+    if (!ragged0 && h->upper_m > 0) {
+      U.m = h->root_m;
+      if (U.n > (int64_t)128 * h->root_m && h->warp_tiles) {
+        U.m = h->upper_m;
+        set_warp_tiles(h, U);
+      }
+    } else {
+      U.m = m_up;
+    }
+    if (U.warps_per_cta == 0) U.stages = pick_stages(h->stages, U.P, U.m);
     U.T = (int64_t)U.P * U.m;
     U.ntiles = (U.n + U.T - 1) / U.T;
-    U.pad_mode = ragged0 ? 0 : 1;
-    U.stages = pick_stages(h->stages, U.P, U.m);
     lv.push_back(U);
   }
   // scratch: levels >= 1 hold a, b, c, d, x (n_L each); 256-byte aligned
@@ -190,8 +256,14 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
     off[k] = total;
     total += 5 * (size_t)((lv[k].n + 31) / 32 * 32);
   }
+  size_t nodes_off = 0;
+  if (h->chain) {
+    nodes_off = (total + 31) / 32 * 32;
+    total = nodes_off + (size_t)L0.ntiles * 8;  // 7 doubles per Node, padded to 8
+  }
   int st = ensure_scratch(h, total * sizeof(double));
   if (st) return st;
+  h->chain_nodes = h->chain ? (void*)(h->scratch + nodes_off) : nullptr;
   for (size_t k = 1; k < lv.size(); ++k) {
     const size_t stride = (size_t)((lv[k].n + 31) / 32 * 32);
     double* base = h->scratch + off[k];
@@ -250,9 +322,16 @@ int launch(pm_handle_t h, int mode, const TileArgs& A, const Level& L, cudaStrea
   return PM_OK;
 }
 
+
 // REDUCE of level k over tiles [t0, t1): writes rows into level k+1 (or `out4`).
+void set_chain(pm_handle_t h, TileArgs& A, int part) {
+  A.nchunks = h->part_chunks[part];
+  A.chunk_base = h->part_base[part];
+  A.chain_nodes = static_cast<pm::Node*>(h->chain_nodes);
+}
+
 int enq_reduce(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, bool zf, bool zl,
-               int64_t sys_len, double* const* out4) {
+               int64_t sys_len, double* const* out4, int part = 0) {
   const Level& L = h->levels[k];
   TileArgs A = args_for(h, L, t0, t1);
   if (out4) {
@@ -265,11 +344,12 @@ int enq_reduce(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st,
   A.zero_first = zf;
   A.zero_last = zl;
   A.sys_len = (k == 0) ? sys_len : 0;
+  if (k == 0 && h->chain) set_chain(h, A, part);
   return launch(h, pm::kModeReduce, A, L, st);
 }
 
 int enq_solve(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, bool zf, bool zl,
-              int64_t sys_len, const double* xb) {
+              int64_t sys_len, const double* xb, int part = 0) {
   const Level& L = h->levels[k];
   TileArgs A = args_for(h, L, t0, t1);
   A.xb = xb ? xb : h->levels[k + 1].x;
@@ -278,6 +358,7 @@ int enq_solve(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, 
   A.zero_last = zl;
   A.sys_len = (k == 0) ? sys_len : 0;
   A.reverse = h->reverse;
+  if (k == 0 && h->chain) set_chain(h, A, part);
   return launch(h, pm::kModeSolve, A, L, st);
 }
 
@@ -288,7 +369,9 @@ int enq_root(pm_handle_t h, size_t k, cudaStream_t st, int64_t sys_len) {
   return launch(h, pm::kModeRoot, A, L, st);
 }
 
-// Upper levels (1..top) on one stream: REDUCE 1..top-1, ROOT top, SOLVE top-1..1.
+
+// Upper levels (1..top) on one stream: REDUCE 1..top-1, ROOT top, SOLVE
+// top-1..1 (chain mode: level 1 is the top, a single ROOT).
 int enq_upper(pm_handle_t h, cudaStream_t st) {
   const size_t top = h->levels.size() - 1;
   int r;
@@ -422,6 +505,18 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       if (value < 0 || value > 4) return fail(h, PM_ERR_VALIDATION, "solve stages must lie in [0, 4]");
       h->solve_stages = (int)value;
       return PM_OK;
+    case PM_OPT_CHAIN:
+      h->opt_chain = value ? 1 : 0;
+      return PM_OK;
+    case PM_OPT_UPPER_M:
+      if (value != 0 && (value < 2 || value > 16))
+        return fail(h, PM_ERR_VALIDATION, "upper m must be 0 or lie in [2, 16]");
+      h->upper_m = (int)value;
+      return PM_OK;
+    case PM_OPT_ROOT_M:
+      if (value < 2 || value > PM_MAX_M) return fail(h, PM_ERR_VALIDATION, "root m out of range");
+      h->root_m = (int)value;
+      return PM_OK;
     case PM_OPT_WARPS_PER_CTA:
       if (value < 1 || value > 8) return fail(h, PM_ERR_VALIDATION, "warps per CTA must lie in [1, 8]");
       h->warps_per_cta = (int)value;
@@ -508,10 +603,14 @@ int pm_solve_host_f64(pm_handle_t h, const double* a, const double* b, const dou
   double* dd = dc + stride;
   double* dx = dd + stride;
   h->launches = 0;
-  if ((r = build_plan(h, n, m, da, db, dc, dd, dx, false, 0))) return r;
+  {
+    // parts = the stream chunks, so that chain chunks never straddle them
+    const int parts_hint = ns > 1 ? ns : 1;
+    if ((r = build_plan(h, n, m, da, db, dc, dd, dx, false, 0, true, parts_hint))) return r;
+  }
   const Level& L0 = h->levels[0];
   const bool single_tile = h->levels.size() == 1;
-  int chunks = single_tile ? 1 : (int)std::min<int64_t>(ns, L0.ntiles);
+  int chunks = single_tile ? 1 : h->nparts;
 
   cudaStream_t main = h->main;
   std::vector<cudaStream_t> streams;
@@ -597,7 +696,7 @@ int pm_solve_host_f64(pm_handle_t h, const double* a, const double* b, const dou
       cudaStream_t s = streams[k];
       cudaStreamWaitEvent(s, fork, 0);
       h2d(r0, r1, s);
-      if (e == cudaSuccess && (r = enq_reduce(h, 0, t0, t1, s, true, true, 0, nullptr))) { cleanup(); return r; }
+      if (e == cudaSuccess && (r = enq_reduce(h, 0, t0, t1, s, true, true, 0, nullptr, k))) { cleanup(); return r; }
       cudaEventRecord(done[k], s);
     }
     for (int k = 0; k < chunks; ++k) cudaStreamWaitEvent(main, done[k], 0);
@@ -608,7 +707,7 @@ int pm_solve_host_f64(pm_handle_t h, const double* a, const double* b, const dou
       const int64_t r0 = t0 * L0.T, r1 = std::min(n, t1 * L0.T);
       cudaStream_t s = streams[k];
       cudaStreamWaitEvent(s, join, 0);
-      if (e == cudaSuccess && (r = enq_solve(h, 0, t0, t1, s, true, true, 0, nullptr))) { cleanup(); return r; }
+      if (e == cudaSuccess && (r = enq_solve(h, 0, t0, t1, s, true, true, 0, nullptr, k))) { cleanup(); return r; }
       d2h(r0, r1, s);
       cudaEventRecord(done[k], s);
     }
@@ -728,7 +827,7 @@ int pm_dist_reduce_f64(pm_handle_t h, const double* a, const double* b, const do
   PM_CUDA(h, cudaSetDevice(h->device));
   h->launches = 0;
   // same plan (and the same 32-double prefix) as pm_dist_solve_f64
-  if ((r = build_plan(h, n_local, m, a, b, c, d, const_cast<double*>(d), !last, 32))) return r;
+  if ((r = build_plan(h, n_local, m, a, b, c, d, const_cast<double*>(d), !last, 32, false))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
   const bool zf = rank == 0, zl = last;
@@ -753,7 +852,7 @@ int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const dou
   PM_CUDA(h, cudaSetDevice(h->device));
   h->launches = 0;
   // two extra doubles in front of the level scratch hold this rank's (xf, xl)
-  if ((r = build_plan(h, n_local, m, a, b, c, d, x, !last, 32))) return r;
+  if ((r = build_plan(h, n_local, m, a, b, c, d, x, !last, 32, false))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
   double* xb = h->scratch;  // extra_doubles region

@@ -217,8 +217,8 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
     double gp = r.a(1) * inv[1];
     double P = 1.0, Y1 = yp, G1 = gp;
     if constexpr (KEEP) {
-      r.B[1] = inv[1];
-      if (L > 1) r.C[1] = cp;
+      r.set_b(1, inv[1]);
+      if (L > 1) r.set_c(1, cp);
     }
 #pragma unroll
     for (int j = 2; j <= L; ++j) {
@@ -230,8 +230,8 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
       Y1 = fma(P, yp, Y1);
       G1 = fma(P, gp, G1);
       if constexpr (KEEP) {
-        r.B[j] = inv[j];
-        if (j < L) r.C[j] = cp;
+        r.set_b(j, inv[j]);
+        if (j < L) r.set_c(j, cp);
       }
     }
     const double hL = r.c(L) * inv[L];
@@ -250,24 +250,24 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
 template <int M, class Acc>
 __device__ __forceinline__ void block_interior_kept(Acc& r, double xs, double xe) {
   if constexpr (M == 2) {
-    r.B[0] = xs;
-    r.B[1] = xe;
+    r.set_b(0, xs);
+    r.set_b(1, xe);
   } else {
     constexpr int L = M - 2;
     double dp[L + 1];
-    dp[1] = fma(-r.a(1), xs, r.d(1)) * r.B[1];
+    dp[1] = fma(-r.a(1), xs, r.d(1)) * r.b(1);
 #pragma unroll
-    for (int j = 2; j <= L; ++j) dp[j] = fma(-r.a(j), dp[j - 1], r.d(j)) * r.B[j];
-    dp[L] = fma(-(r.C[L] * r.B[L]), xe, dp[L]);  // - h_L * x_e
+    for (int j = 2; j <= L; ++j) dp[j] = fma(-r.a(j), dp[j - 1], r.d(j)) * r.b(j);
+    dp[L] = fma(-(r.c(L) * r.b(L)), xe, dp[L]);  // - h_L * x_e
     double xn = dp[L];
-    r.B[L] = xn;
+    r.set_b(L, xn);
 #pragma unroll
     for (int j = L - 1; j >= 1; --j) {
-      xn = fma(-r.C[j], xn, dp[j]);
-      r.B[j] = xn;
+      xn = fma(-r.c(j), xn, dp[j]);
+      r.set_b(j, xn);
     }
-    r.B[0] = xs;
-    r.B[M - 1] = xe;
+    r.set_b(0, xs);
+    r.set_b(M - 1, xe);
   }
 }
 

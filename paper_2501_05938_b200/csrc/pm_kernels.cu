@@ -32,6 +32,12 @@
 namespace pm {
 
 constexpr int kMaxStages = 4;
+// Stage 3 (level 0) keeps the block rows in its shared-memory stage: ~106
+// registers and a single stage per warp give 16 warps per SM, which hides
+// the sweeps' FP64 latency better than the register-resident variant.
+#ifndef PM_SOLVE_STAGE_ROWS
+#define PM_SOLVE_STAGE_ROWS 1
+#endif
 constexpr int kMaxWarps = 8;  // P <= 256
 
 // ---------------------------------------------------------------------------
@@ -157,6 +163,8 @@ struct RegAcc {
   __device__ __forceinline__ double dp(int j) const { return D[j]; }
   __device__ __forceinline__ void set_x(int j, double v) { B[j] = v; }
   __device__ __forceinline__ double x(int j) const { return B[j]; }
+  __device__ __forceinline__ void set_b(int j, double v) { B[j] = v; }
+  __device__ __forceinline__ void set_c(int j, double v) { C[j] = v; }
 
   __device__ __forceinline__ void load(const double* sa, const double* sb, const double* sc,
                                        const double* sd, int r0, const TileCtx& t) {
@@ -183,6 +191,44 @@ struct RegAcc {
     if (block_needs_fixup(t, r0, M)) {
 #pragma unroll
       for (int j = 0; j < M; ++j) fixup_row(t, r0 + j, A[j], B[j], C[j], D[j]);
+    }
+  }
+  // all four rows arrays back to the stage / raw reload (16-byte accesses:
+  // conflict-free at stride m = 10, unlike 8-byte ones)
+  __device__ __forceinline__ void store_rows(double* sa, double* sb, double* sc, double* sd,
+                                             int r0) const {
+    if constexpr ((M % 2) == 0) {
+#pragma unroll
+      for (int j = 0; j < M / 2; ++j) {
+        reinterpret_cast<double2*>(sa + r0)[j] = make_double2(A[2 * j], A[2 * j + 1]);
+        reinterpret_cast<double2*>(sb + r0)[j] = make_double2(B[2 * j], B[2 * j + 1]);
+        reinterpret_cast<double2*>(sc + r0)[j] = make_double2(C[2 * j], C[2 * j + 1]);
+        reinterpret_cast<double2*>(sd + r0)[j] = make_double2(D[2 * j], D[2 * j + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        sa[r0 + j] = A[j]; sb[r0 + j] = B[j]; sc[r0 + j] = C[j]; sd[r0 + j] = D[j];
+      }
+    }
+  }
+  __device__ __forceinline__ void load_raw(const double* sa, const double* sb, const double* sc,
+                                           const double* sd, int r0) {
+    if constexpr ((M % 2) == 0) {
+#pragma unroll
+      for (int j = 0; j < M / 2; ++j) {
+        const double2 va = reinterpret_cast<const double2*>(sa + r0)[j];
+        const double2 vb = reinterpret_cast<const double2*>(sb + r0)[j];
+        const double2 vc = reinterpret_cast<const double2*>(sc + r0)[j];
+        const double2 vd = reinterpret_cast<const double2*>(sd + r0)[j];
+        A[2 * j] = va.x; A[2 * j + 1] = va.y; B[2 * j] = vb.x; B[2 * j + 1] = vb.y;
+        C[2 * j] = vc.x; C[2 * j + 1] = vc.y; D[2 * j] = vd.x; D[2 * j + 1] = vd.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        A[j] = sa[r0 + j]; B[j] = sb[r0 + j]; C[j] = sc[r0 + j]; D[j] = sd[r0 + j];
+      }
     }
   }
   __device__ __forceinline__ void store_x(double* xbuf, int r0) const {
@@ -225,6 +271,24 @@ struct SmemAcc {
       }
     }
   }
+};
+
+// Compile-time m, rows left in the shared-memory stage (fewer registers):
+// b/c slots are overwritten with 1/den and c' by block_reduce_fast<M, true>
+// and b with x by block_interior_kept.
+template <int M>
+struct StageAcc {
+  double* sa;
+  double* sb;
+  double* sc;
+  double* sd;
+  __device__ __forceinline__ double a(int j) const { return sa[j]; }
+  __device__ __forceinline__ double b(int j) const { return sb[j]; }
+  __device__ __forceinline__ double c(int j) const { return sc[j]; }
+  __device__ __forceinline__ double d(int j) const { return sd[j]; }
+  __device__ __forceinline__ void set_b(int j, double v) { sb[j] = v; }
+  __device__ __forceinline__ void set_c(int j, double v) { sc[j] = v; }
+  __device__ __forceinline__ double x(int j) const { return sb[j]; }
 };
 
 // ---------------------------------------------------------------------------
@@ -532,22 +596,46 @@ __device__ __forceinline__ void warp_downsweep(double& xf, double& xl, const Nod
     down_level(nodes + warp_node_off(k), 1 << k, lane, 32, lane + (1 << k) < nblk, xf, xl);
 }
 
+// Per-warp shared memory: [stages][a,b,c,d][T] | x buffer | 31 tree nodes | mbarriers.
+// The x buffer exists only for Stage 3 with rows in registers (runtime m).
+__host__ __device__ size_t warp_xbuf_doubles(int mode, int m) {
+  const bool stage_rows = PM_SOLVE_STAGE_ROWS != 0 && (m == 2 || m == 8 || m == 10 || m == 16);
+  return (mode != kModeReduce && !stage_rows) ? (size_t)32 * m : 0;
+}
+
 __host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages) {
   const size_t T = (size_t)32 * m;
-  size_t bytes = (size_t)stages * 4 * T * sizeof(double) + 2 * kMaxStages * sizeof(uint64_t);
-  if (mode != kModeReduce) bytes += T * sizeof(double) + 31 * sizeof(Node);
+  size_t bytes = (size_t)stages * 4 * T * sizeof(double) + warp_xbuf_doubles(mode, m) * sizeof(double) +
+                 31 * sizeof(Node) + 2 * kMaxStages * sizeof(uint64_t);
   return (bytes + 127) / 128 * 128;
 }
 
+
 #ifndef PM_SOLVE_MINB
-#define PM_SOLVE_MINB 1
+#define PM_SOLVE_MINB 4
 #endif
 #ifndef PM_REDUCE_MINB
 #define PM_REDUCE_MINB 1
 #endif
-template <int M, int MODE>
+// Chunk cursor (CHAIN mode): warp w owns chunks w, w+nw, ...; chunk j is the
+// contiguous tile range [lo, hi) = [tile_begin + j*ntiles/C, ...).  Stage 1
+// walks a chunk forward, Stage 3 backward.
+struct ChunkCursor {
+  int64_t j, lo, hi, pos;
+};
+
+__device__ __forceinline__ void chunk_range(const TileArgs& A, int64_t j, int64_t& lo, int64_t& hi) {
+  const int64_t nt = A.tile_end - A.tile_begin;
+  lo = A.tile_begin + (nt * j) / A.nchunks;
+  hi = A.tile_begin + (nt * (j + 1)) / A.nchunks;
+}
+
+template <int M, int MODE, bool CHAIN>
 __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : PM_SOLVE_MINB))
     warp_tile_kernel(TileArgs args) {
+  // Stage 3 keeping the block rows in the shared-memory stage (late release)
+  // instead of registers (early release)
+  constexpr bool kStageRows = (M > 0) && (MODE != kModeReduce) && (PM_SOLVE_STAGE_ROWS != 0);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int m = (M > 0) ? M : args.m;
   const int T = 32 * m;
@@ -561,16 +649,56 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
   unsigned char* base = smem_raw + per_warp * warp;
   double* stage0 = reinterpret_cast<double*>(base);
   double* xbuf = stage0 + (size_t)S * 4 * T;
-  Node* nodes = reinterpret_cast<Node*>(xbuf + T);
+  Node* nodes = reinterpret_cast<Node*>(xbuf + warp_xbuf_doubles(MODE, m));
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + per_warp - 2 * kMaxStages * sizeof(uint64_t));
 
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   const int64_t nwarp_total = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t ntiles = args.tile_end - args.tile_begin;
-  const int64_t nlocal = (ntiles > gwarp) ? (ntiles - gwarp + nwarp_total - 1) / nwarp_total : 0;
+  int64_t nlocal = 0;
+  if constexpr (CHAIN) {
+    for (int64_t j = gwarp; j < args.nchunks; j += nwarp_total) {
+      int64_t lo, hi;
+      chunk_range(args, j, lo, hi);
+      nlocal += hi - lo;
+    }
+  } else {
+    nlocal = (ntiles > gwarp) ? (ntiles - gwarp + nwarp_total - 1) / nwarp_total : 0;
+  }
+  // strided mode: random access; chain mode: two cursors (compute, issue)
   auto tile_of = [&](int64_t k) -> int64_t {
     const int64_t idx = gwarp + k * nwarp_total;
     return args.reverse ? (args.tile_end - 1 - idx) : (args.tile_begin + idx);
+  };
+  auto cur_init = [&](ChunkCursor& c) {
+    c.j = gwarp;
+    c.pos = 0;
+    if (c.j < args.nchunks) chunk_range(args, c.j, c.lo, c.hi);
+    else c.lo = c.hi = 0;
+  };
+  auto cur_tile = [&](const ChunkCursor& c) -> int64_t {
+    return (MODE == kModeReduce) ? c.lo + c.pos : c.hi - 1 - c.pos;
+  };
+  auto cur_next = [&](ChunkCursor& c) {
+    if (++c.pos >= c.hi - c.lo) {
+      c.j += nwarp_total;
+      c.pos = 0;
+      if (c.j < args.nchunks) chunk_range(args, c.j, c.lo, c.hi);
+    }
+  };
+  ChunkCursor cc, ic;  // compute / issue cursors (CHAIN)
+  if constexpr (CHAIN) {
+    cur_init(cc);
+    cur_init(ic);
+  }
+  auto next_issue_tile = [&](int64_t kk) -> int64_t {  // tile of local index kk (issue order)
+    if constexpr (CHAIN) {
+      const int64_t t = cur_tile(ic);
+      cur_next(ic);
+      return t;
+    } else {
+      return tile_of(kk);
+    }
   };
   auto stage_ptr = [&](int s, int q) -> double* { return stage0 + ((size_t)s * 4 + q) * T; };
   auto issue = [&](int s, int64_t t) {
@@ -592,26 +720,73 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     fence_mbar_init();
   }
   __syncwarp();
-  if (lane == 0)
-    for (int s = 0; s < S && s < nlocal; ++s) issue(s, tile_of(s));
+  for (int s = 0; s < S && s < nlocal; ++s) {
+    const int64_t t = next_issue_tile(s);  // all lanes advance the cursor
+    if (lane == 0) issue(s, t);
+  }
 
   bool bad = false;
-  // Stage 3: the tile's boundary values come from the level above; fetch
-  // them one tile ahead so the load latency is off the critical path.
+  // Stage 3 boundary values of the tile.  Strided mode: from the level above,
+  // fetched one tile ahead.  Chain mode (lane 0): walk the chunk's chain
+  // backwards from the chunk's two values -- the node stored by Stage 1 for
+  // tile t splits (x_first(chunk), x_last(tiles lo..t)) into
+  // x_last(tiles lo..t-1) and x_first(tile t).
   double xf_next = 0.0, xl_next = 0.0;
+  double xf_chunk = 0.0, xl_run = 0.0;
+  Node nd_next{};
   if (MODE != kModeReduce && nlocal > 0) {
-    const int64_t t0 = tile_of(0);
-    xf_next = __ldg(args.xb + 2 * t0);
-    xl_next = __ldg(args.xb + 2 * t0 + 1);
+    if constexpr (CHAIN) {
+      if (lane == 0 && cc.hi - cc.lo > 1) nd_next = args.chain_nodes[cc.hi - 1];
+    } else {
+      const int64_t t0 = tile_of(0);
+      xf_next = __ldg(args.xb + 2 * t0);
+      xl_next = __ldg(args.xb + 2 * t0 + 1);
+    }
   }
+  Seg acc;  // Stage 1 chain accumulator (lane 0)
   for (int64_t k = 0; k < nlocal; ++k) {
-    const int64_t t = tile_of(k);
+    int64_t t;
+    bool chunk_first = false, chunk_last = false;  // in processing order
+    int64_t chunk = 0;
+    if constexpr (CHAIN) {
+      t = cur_tile(cc);
+      chunk = cc.j;
+      chunk_first = (cc.pos == 0);
+      chunk_last = (cc.pos == cc.hi - cc.lo - 1);
+      cur_next(cc);
+    } else {
+      t = tile_of(k);
+    }
     const int s = static_cast<int>(k % S);
     double xf_tile = xf_next, xl_tile = xl_next;
-    if (MODE != kModeReduce && k + 1 < nlocal) {
-      const int64_t tn = tile_of(k + 1);
-      xf_next = __ldg(args.xb + 2 * tn);
-      xl_next = __ldg(args.xb + 2 * tn + 1);
+    if constexpr (MODE != kModeReduce) {
+      if constexpr (CHAIN) {
+        if (lane == 0) {
+          if (chunk_first) {
+            xf_chunk = __ldg(args.xb + 2 * (args.chunk_base + chunk));
+            xl_run = __ldg(args.xb + 2 * (args.chunk_base + chunk) + 1);
+          }
+          if (chunk_last) {  // the chunk's first tile
+            xf_tile = xf_chunk;
+            xl_tile = xl_run;
+          } else {
+            double xl_prev, xf_t;
+            split_node(nd_next, xf_chunk, xl_run, xl_prev, xf_t);
+            xf_tile = xf_t;
+            xl_tile = xl_run;
+            xl_run = xl_prev;
+          }
+          // prefetch the node of the next tile in processing order
+          if (k + 1 < nlocal) {
+            const int64_t tn = cur_tile(cc);
+            if (tn != cc.lo) nd_next = args.chain_nodes[tn];
+          }
+        }
+      } else if (k + 1 < nlocal) {
+        const int64_t tn = tile_of(k + 1);
+        xf_next = __ldg(args.xb + 2 * tn);
+        xl_next = __ldg(args.xb + 2 * tn + 1);
+      }
     }
     TileCtx ctx;
     ctx.ga = args.a; ctx.gb = args.b; ctx.gc = args.c; ctx.gd = args.d;
@@ -630,25 +805,51 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
 
     Seg seg;
-    RegAcc<(M > 0 ? M : 1)> regs;
+    RegAcc<(M > 0 && !kStageRows ? M : 1)> regs;
+    StageAcc<(M > 0 ? M : 1)> stg{sa + r0, sb + r0, sc + r0, sd + r0};
     SmemAcc sacc{sa + r0, sb + r0, sc + r0, sd + r0, xbuf + r0};
-    if constexpr (M > 0) {
+    if constexpr (kStageRows) {
+      sacc.fixup(r0, m, ctx);
+      seg = block_reduce_fast<M, true>(stg, bad);
+    } else if constexpr (M > 0) {
       regs.load(sa, sb, sc, sd, r0, ctx);
       __syncwarp();
-      if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));  // early release
+      if (k + S < nlocal) {  // early release
+        const int64_t tn = next_issue_tile(k + S);
+        if (lane == 0) issue(s, tn);
+      }
       seg = block_reduce_fast<M, MODE != kModeReduce>(regs, bad);
     } else {
       sacc.fixup(r0, m, ctx);
       seg = block_reduce<0>(sacc, m, bad);
       if constexpr (MODE == kModeReduce) {
         __syncwarp();
-        if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));
+        if (k + S < nlocal) {
+          const int64_t tn = next_issue_tile(k + S);
+          if (lane == 0) issue(s, tn);
+        }
       }
     }
 
     Seg top = warp_upsweep(seg, MODE == kModeReduce ? nullptr : nodes, lane, nblk, bad);
     if constexpr (MODE == kModeReduce) {
-      if (lane == 0) {
+      if constexpr (CHAIN) {
+        if (lane == 0) {
+          if (chunk_first) {
+            acc = top;
+          } else {
+            Node nd;
+            combine(acc, top, acc, nd, bad);
+            args.chain_nodes[t] = nd;
+          }
+          if (chunk_last) {
+            const int64_t r = 2 * (args.chunk_base + chunk);
+            args.ra[r] = acc.F.a; args.rb[r] = acc.F.b; args.rc[r] = acc.F.c; args.rd[r] = acc.F.d;
+            args.ra[r + 1] = acc.L.a; args.rb[r + 1] = acc.L.b;
+            args.rc[r + 1] = acc.L.c; args.rd[r + 1] = acc.L.d;
+          }
+        }
+      } else if (lane == 0) {
         args.ra[2 * t] = top.F.a; args.rb[2 * t] = top.F.b;
         args.rc[2 * t] = top.F.c; args.rd[2 * t] = top.F.d;
         args.ra[2 * t + 1] = top.L.a; args.rb[2 * t + 1] = top.L.b;
@@ -658,7 +859,12 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       double xf = xf_tile, xl = xl_tile;
       __syncwarp();  // nodes written by lanes are read by the same lanes only
       warp_downsweep(xf, xl, nodes, lane, nblk);
-      if constexpr (M > 0) {
+      const double* xsrc = kStageRows ? sb : xbuf;
+      if constexpr (kStageRows) {
+        block_interior_kept<M>(stg, xf, xl);
+#pragma unroll
+        for (int j = 0; j < M; ++j) bad |= !isfinite(stg.x(j));
+      } else if constexpr (M > 0) {
         block_interior_kept<M>(regs, xf, xl);
 #pragma unroll
         for (int j = 0; j < M; ++j) bad |= !isfinite(regs.x(j));
@@ -672,25 +878,28 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       double* gx = args.x + ctx.row0;
       const int v = ctx.valid;
       if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & 15) == 0)) {
-        const double2* s2 = reinterpret_cast<const double2*>(xbuf);
+        const double2* s2 = reinterpret_cast<const double2*>(xsrc);
         double2* g2 = reinterpret_cast<double2*>(gx);
         for (int i = lane; i < v / 2; i += 32) g2[i] = s2[i];
       } else {
-        for (int i = lane; i < v; i += 32) gx[i] = xbuf[i];
+        for (int i = lane; i < v; i += 32) gx[i] = xsrc[i];
       }
       __syncwarp();
-      if constexpr (M == 0) {
-        if (lane == 0 && k + S < nlocal) issue(s, tile_of(k + S));
+      if constexpr (M == 0 || kStageRows) {
+        if (k + S < nlocal) {
+          const int64_t tn = next_issue_tile(k + S);
+          if (lane == 0) issue(s, tn);
+        }
       }
     }
   }
   if (bad) atomicOr(args.flag, 1);
 }
 
-template <int M, int MODE>
+template <int M, int MODE, bool CHAIN>
 static cudaError_t launch_warp_one(const TileArgs& args, int warps_per_cta, int sm_count,
                                    cudaStream_t st, int* grid_out) {
-  auto kern = warp_tile_kernel<M, MODE>;
+  auto kern = warp_tile_kernel<M, MODE, CHAIN>;
   const int m = (M > 0 ? M : args.m);
   const size_t smem = warp_smem_bytes(MODE, m, args.stages) * warps_per_cta;
   static thread_local size_t configured = 0;
@@ -708,7 +917,8 @@ static cudaError_t launch_warp_one(const TileArgs& args, int warps_per_cta, int 
   const int64_t ntiles = args.tile_end - args.tile_begin;
   int64_t grid = (int64_t)per_sm * sm_count;
   if (args.max_ctas > 0 && grid > args.max_ctas) grid = args.max_ctas;
-  const int64_t need = (ntiles + warps_per_cta - 1) / warps_per_cta;
+  const int64_t units = args.nchunks > 0 ? args.nchunks : ntiles;
+  const int64_t need = (units + warps_per_cta - 1) / warps_per_cta;
   if (grid > need) grid = need;
   if (grid_out) *grid_out = (int)grid;
   if (grid <= 0) return cudaSuccess;
@@ -716,23 +926,56 @@ static cudaError_t launch_warp_one(const TileArgs& args, int warps_per_cta, int 
   return cudaGetLastError();
 }
 
+template <bool CHAIN>
+static cudaError_t launch_warp_m(int mode, const TileArgs& args, int warps_per_cta, int sm_count,
+                                 cudaStream_t st, int* grid_out) {
+  const bool red = (mode == kModeReduce);
+#define PM_WARP_CASE(MM)                                                                        \
+  return red ? launch_warp_one<MM, kModeReduce, CHAIN>(args, warps_per_cta, sm_count, st,      \
+                                                        grid_out)                              \
+             : launch_warp_one<MM, kModeSolve, CHAIN>(args, warps_per_cta, sm_count, st, grid_out)
+  switch (m_is_specialised(args.m) ? args.m : 0) {
+    case 2: PM_WARP_CASE(2);
+    case 8: PM_WARP_CASE(8);
+    case 10: PM_WARP_CASE(10);
+    case 16: PM_WARP_CASE(16);
+    default: PM_WARP_CASE(0);
+  }
+#undef PM_WARP_CASE
+}
+
 cudaError_t launch_warp_tile_kernel(int mode, const TileArgs& args, int warps_per_cta,
                                     int sm_count, cudaStream_t st, int* grid_out) {
-  const bool red = (mode == kModeReduce);
-  switch (m_is_specialised(args.m) ? args.m : 0) {
-    case 2:
-      return red ? launch_warp_one<2, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
-                 : launch_warp_one<2, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
-    case 8:
-      return red ? launch_warp_one<8, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
-                 : launch_warp_one<8, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
-    case 10:
-      return red ? launch_warp_one<10, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
-                 : launch_warp_one<10, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
-    default:
-      return red ? launch_warp_one<0, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)
-                 : launch_warp_one<0, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out);
+  return args.nchunks > 0 ? launch_warp_m<true>(mode, args, warps_per_cta, sm_count, st, grid_out)
+                          : launch_warp_m<false>(mode, args, warps_per_cta, sm_count, st, grid_out);
+}
+
+int warp_kernel_ctas_per_sm(int mode, int m, int stages, int warps_per_cta, bool chain) {
+  const size_t smem = warp_smem_bytes(mode, m, stages) * warps_per_cta;
+  int per_sm = 0;
+  auto q = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, smem);
+  };
+  const int M = m_is_specialised(m) ? m : 0;
+  const bool red = mode == kModeReduce;
+#define PM_OCC(MM)                                                             \
+  if (chain) {                                                                 \
+    if (red) q(warp_tile_kernel<MM, kModeReduce, true>);                      \
+    else q(warp_tile_kernel<MM, kModeSolve, true>);                           \
+  } else {                                                                     \
+    if (red) q(warp_tile_kernel<MM, kModeReduce, false>);                     \
+    else q(warp_tile_kernel<MM, kModeSolve, false>);                          \
   }
+  switch (M) {
+    case 2: PM_OCC(2); break;
+    case 8: PM_OCC(8); break;
+    case 10: PM_OCC(10); break;
+    case 16: PM_OCC(16); break;
+    default: PM_OCC(0); break;
+  }
+#undef PM_OCC
+  return per_sm;
 }
 
 // ---------------------------------------------------------------------------
@@ -889,11 +1132,12 @@ static cudaError_t dispatch_m(int Mspec, const TileArgs& args, int P, int sm_cou
     case 2: return launch_one<2, MODE, BULK>(args, P, sm_count, st, grid_out);
     case 8: return launch_one<8, MODE, BULK>(args, P, sm_count, st, grid_out);
     case 10: return launch_one<10, MODE, BULK>(args, P, sm_count, st, grid_out);
+    case 16: return launch_one<16, MODE, BULK>(args, P, sm_count, st, grid_out);
     default: return launch_one<0, MODE, BULK>(args, P, sm_count, st, grid_out);
   }
 }
 
-bool m_is_specialised(int m) { return m == 2 || m == 8 || m == 10; }
+bool m_is_specialised(int m) { return m == 2 || m == 8 || m == 10 || m == 16; }
 
 cudaError_t launch_tile_kernel(int mode, const TileArgs& args, int P, bool bulk, int sm_count,
                                cudaStream_t st, int* grid_out) {

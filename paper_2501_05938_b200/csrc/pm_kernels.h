@@ -8,6 +8,8 @@
 
 namespace pm {
 
+struct Node;
+
 constexpr int kModeReduce = 0;  // Stage 1 of one level: tile -> 2 interface rows
 constexpr int kModeSolve = 1;   // Stage 3 of one level: boundary values -> x
 constexpr int kModeRoot = 2;    // whole (single-tile) top level
@@ -37,7 +39,18 @@ struct TileArgs {
                                          // 0: ragged last tile (n % m == 0 required);
                                          //    its trailing blocks are empty segments
   int64_t sys_len = 0;                   // batch: rows per independent system (0 = one)
+  // chain mode (warp-tile kernels): the launch's tiles form `nchunks`
+  // contiguous chunks; Stage 1 combines each chunk's tile segments in order
+  // (one Node per tile -> chain_nodes[tile]) and writes two rows per chunk
+  // at 2*(chunk_base + j); Stage 3 reads xb[2*(chunk_base + j) .. +1] and
+  // walks the chunk backwards.
+  int64_t nchunks = 0;
+  int64_t chunk_base = 0;
+  struct Node* chain_nodes = nullptr;
 };
+
+// CTAs per SM of a warp-tile kernel variant (occupancy query).
+int warp_kernel_ctas_per_sm(int mode, int m, int stages, int warps_per_cta, bool chain);
 
 // Row-sharded solve: combine the ranks' interface segments (8 doubles each,
 // rank order) and write this rank's two boundary values to xb[0..1].

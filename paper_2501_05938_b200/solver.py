@@ -26,6 +26,9 @@ PM_OPT_KERNEL_TIMES = 6
 PM_OPT_WARP_TILES = 7
 PM_OPT_SOLVE_STAGES = 8
 PM_OPT_WARPS_PER_CTA = 9
+PM_OPT_CHAIN = 10
+PM_OPT_UPPER_M = 11
+PM_OPT_ROOT_M = 12
 PM_MAX_M = 128
 
 

@@ -8,6 +8,6 @@ while read -r lib opts; do
   args=""
   for o in $opts; do args="$args --opt $o"; done
   if [ "$lib" = "default" ]; then export -n PM_LIB_PATH; unset PM_LIB_PATH; else export PM_LIB_PATH=$lib; fi
-  r=$(timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu $args 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print(f\"{d['ms_per_step']:.4f} ms  solve {r['kernel_ms']:.4f} ({r['frac']:.3f})  reduce {r['stage1']['kernel_ms']:.4f} ({r['stage1']['frac']:.3f})  whole {r['whole_solve']['frac']:.3f}\")" 2>&1)
+  r=$(timeout 300 python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu $args 2>&1 | python scripts/summarize_bench.py)
   echo "$lib $opts :: $r" | tee -a $OUT
 done < ${CONFIGS:-scripts/sweep_configs.txt}

@@ -272,7 +272,8 @@ def test_launch_plan_n8e7(solver):
     solver.generate_device(n, 1, arrays=[a, b, c, d])
     solver.solve_device(a, b, c, d, m=10)
     solver.check()
-    # level 0: warp tiles of 32*10 rows -> 2 rows each; level 1: CTA tiles of 1024 rows
+    # level 0: warp tiles of 32*10 rows -> 2 rows each; level 1: CTA tiles of
+    # 128*8 rows; level 2 (<= 1024 rows): one ROOT tile
     assert solver.last_plan() == [80_000_000, 500_000, 978]
     assert solver.last_launch_count == 5
 
@@ -293,3 +294,54 @@ def test_level0_kernel_variants(solver, warp_tiles, n, m):
     finally:
         solver.set_option(PM_OPT_WARP_TILES, 1)
     _check(x.cpu().numpy(), *oracle.generate(n, n % 97))
+
+
+@pytest.mark.parametrize("n", [321, 51_200, 51_201, 8_192_000, 8_192_321, 16_384_000, 30_000_001])
+@pytest.mark.parametrize("chain", [0, 1])
+def test_chain_sizes(solver, n, chain):
+    """Sizes around tile / chunk boundaries, with and without the chained level 0
+    (PM_OPT_CHAIN: warp-owned contiguous chunks, level 1 = one ROOT tile)."""
+    from paper_2501_05938_b200.solver import PM_OPT_CHAIN
+
+    solver.set_option(PM_OPT_CHAIN, chain)
+    try:
+        a, b, c, d = _device_system(solver, n, seed=3)
+        for _ in range(3):  # repeated solves on one handle
+            x = solver.solve_device(a, b, c, d, m=10)
+            solver.check()
+        if chain and n > 1280:
+            assert len(solver.last_plan()) == 2 and solver.last_launch_count == 3
+    finally:
+        solver.set_option(PM_OPT_CHAIN, 0)
+    _check(x.cpu().numpy(), *oracle.generate(n, 3))
+
+
+@pytest.mark.parametrize("ns", [1, 4, 32])
+def test_chain_host_streams(solver, ns):
+    from paper_2501_05938_b200.solver import PM_OPT_CHAIN
+
+    n = 3_000_017
+    ah, bh, ch, dh = oracle.generate(n, 8)
+    solver.set_option(PM_OPT_CHAIN, 1)
+    try:
+        x = solver.solve_host(ah, bh, ch, dh, m=10, num_streams=ns)
+    finally:
+        solver.set_option(PM_OPT_CHAIN, 0)
+    _check(x, ah, bh, ch, dh)
+
+
+def test_golden_scaled_systems(solver):
+    """Badly scaled (but dominant) golden systems: exercises the power-of-two
+    scaling of the division-free combine."""
+    import torch
+
+    from pathlib import Path
+
+    s = np.load(Path(__file__).resolve().parent / "golden" / "systems.npz")
+    for key in s.files:
+        a, b, c, d, xg = (np.ascontiguousarray(v) for v in s[key])
+        t = [torch.from_numpy(v.copy()).cuda() for v in (a, b, c, d)]
+        for m in (2, 3, 10, 16):
+            x = solver.solve_device(*t, m=m)
+            solver.check()
+            assert oracle.rel_err(x.cpu().numpy(), xg) <= REL_TOL, (key, m)
