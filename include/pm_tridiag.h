@@ -138,6 +138,8 @@ int pm_get_model_bundle(pm_handle_t h, pm_model_bundle* out);
  * Returns the stream count (>= 1) or -1 on a validation error. */
 int pm_recommend_streams(int64_t n, const pm_model_bundle* bundle);
 int pm_paper_bundle(pm_model_bundle* out);
+/* The B200 re-fit (tools/refit.py): a new handle's default bundle. */
+int pm_b200_bundle(pm_model_bundle* out);
 
 /* Counter-based synthetic system (bit-identical to the CPU oracle's
  * generator): a, c ~ U(-1,1) with a[0] = c[n-1] = 0, b = +-(|a|+|c|+1+U(0,1)),

@@ -34,6 +34,10 @@ struct ModelBundle {
   // The RTX 2080 Ti bundle published in the paper: Eq. 4 and
   // Eq. 7.
   static ModelBundle paper();
+
+  // The same model forms re-fitted on an NVIDIA B200 with this solver
+  // (tools/refit.py, data in refit/pooled/): the C ABI's default bundle.
+  static ModelBundle b200();
 };
 
 enum class OverheadModel { small, big };

@@ -50,6 +50,7 @@ PM_SIGNATURES = [
     ("pm_get_model_bundle", C.c_int, [C.c_void_p, C.POINTER(ModelBundleC)]),
     ("pm_recommend_streams", C.c_int, [C.c_int64, C.POINTER(ModelBundleC)]),
     ("pm_paper_bundle", C.c_int, [C.POINTER(ModelBundleC)]),
+    ("pm_b200_bundle", C.c_int, [C.POINTER(ModelBundleC)]),
     ("pm_generate_f64", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_uint64, C.c_void_p]),
     ("pm_dist_reduce_f64", C.c_int,
      [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),

@@ -84,7 +84,7 @@ struct pm_handle_s {
   std::vector<cudaStream_t> pool;
   cudaStream_t main = nullptr;
   cudaStream_t last_stream = nullptr;
-  streamtune::ModelBundle bundle = streamtune::ModelBundle::paper();
+  streamtune::ModelBundle bundle = streamtune::ModelBundle::b200();
   pm_stage_timings last_t{};
   double last_total_ms = 0.0;
   int last_streams = 0;
@@ -780,6 +780,12 @@ int pm_get_model_bundle(pm_handle_t h, pm_model_bundle* out) {
 int pm_paper_bundle(pm_model_bundle* out) {
   if (!out) return PM_ERR_VALIDATION;
   to_c(streamtune::ModelBundle::paper(), out);
+  return PM_OK;
+}
+
+int pm_b200_bundle(pm_model_bundle* out) {
+  if (!out) return PM_ERR_VALIDATION;
+  to_c(streamtune::ModelBundle::b200(), out);
   return PM_OK;
 }
 

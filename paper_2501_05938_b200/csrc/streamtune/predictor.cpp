@@ -34,6 +34,13 @@ ModelBundle ModelBundle::paper() {
   return b;
 }
 
+ModelBundle ModelBundle::b200() {
+  ModelBundle b;
+#include "b200_bundle.inc"
+  b.fitted_on = "NVIDIA B200 re-fit (tools/refit.py; refit/pooled/)";
+  return b;
+}
+
 double predict_sum(const ModelBundle& bundle, std::uint64_t slae_size) {
   return bundle.sum_a * static_cast<double>(slae_size) + bundle.sum_b;
 }

@@ -58,6 +58,12 @@ class ModelBundle:
         return ModelBundle.from_c(c, provenance={"fitted_on": "RTX 2080 Ti (paper Eq. 4 / Eq. 7)"})
 
     @staticmethod
+    def b200() -> "ModelBundle":
+        c = ModelBundleC()
+        _lib.load().pm_b200_bundle(C.byref(c))
+        return ModelBundle.from_c(c, provenance={"fitted_on": "NVIDIA B200 re-fit (refit/pooled/)"})
+
+    @staticmethod
     def from_c(c, provenance=None) -> "ModelBundle":
         return ModelBundle(c.sum_a, c.sum_b, c.small_a, c.small_b, c.small_c, c.big_a, c.big_b, c.big_c,
                            int(c.size_threshold), tuple(c.candidates[k] for k in range(c.num_candidates)),

@@ -313,3 +313,29 @@ def test_fit_bundle_recovers_paper_coefficients():
     assert met["sum"]["train"]["r_squared"] > 0.999999
     with pytest.raises(errors.TooFewObservationsError):
         st.fit_bundle(stage, RUNS_HDR + "1000,1,1.0\n")
+
+
+def test_b200_refit_bundle_matches_committed_sweep():
+    """The compiled-in B200 bundle is the fit of the committed sweep data
+    (refit/pooled/, tools/refit.py) and reproduces its validation."""
+    import json
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1] / "refit" / "pooled"
+    stage = (root / "stage_timings.csv").read_text()
+    runs = (root / "streamed_runs.csv").read_text()
+    fitted, _ = st.fit_bundle(stage, runs)
+    b = st.ModelBundle.b200()
+    for k in ("sum_a", "sum_b", "small_a", "small_b", "small_c", "big_a", "big_b", "big_c"):
+        assert getattr(b, k) == pytest.approx(getattr(fitted, k), rel=1e-12, abs=1e-15), k
+    val = json.loads((root / "validation.json").read_text())
+    assert val["sizes"] == 30
+    for row in val["rows"]:
+        assert st.recommend(b, row["slae_size"]).chosen == row["predicted"]
+    # north_star bar: predicted count within one power of two of the measured optimum
+    assert val["within_one_power_of_two"] >= 28
+    from paper_2501_05938_b200 import _lib
+    import ctypes as C
+
+    c = _lib.ModelBundleC()
+    assert _lib.load().pm_b200_bundle(C.byref(c)) == 0 and c.sum_a == b.sum_a

@@ -1,0 +1,176 @@
+#!/usr/bin/env python
+"""B200 re-fit of the paper's stream-count models (BASELINE.json config 2).
+
+The C2 sweep: 30 SLAE sizes {1, 2.5, 4, 5, 7.5, 8} x 10^i, i = 3..7, m = 10,
+num_streams in {1, 2, 4, 8, 16, 32}, end to end through pm_solve_host_f64
+from page-locked host buffers (PAPER.md:52 sizes; PAPER.md:60 counts).
+
+1. StageTimings per size, measured unstreamed with CUDA events
+   (PM_OPT_TIMINGS; t1_d2h = t3_h2d = 0 because the reduced system never
+   leaves the device, t2_comp = the GPU reduced solve).
+2. T_str per (size, n): median of `reps` solves (the handle's event total).
+3. The two CSV documents of SPEC.md:349/359 are written and fed to the C++
+   fit (st_fit_bundle = cmd_fit: Eq. 4 sum model, Eq. 7
+   small/big overhead models, 3:1 split, seed 42).
+4. Validation: for every size, the bundle's recommend() vs the measured
+   optimum; the north_star bar is "within one power of two".
+
+Outputs (default --out refit/): stage_timings.csv, streamed_runs.csv,
+bundle.json (SPEC.md:316 keys), validation.json; --install also writes
+paper_2501_05938_b200/csrc/streamtune/b200_bundle.inc, the compiled-in
+default of the C ABI's predictor.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import time
+from pathlib import Path
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from paper_2501_05938_b200 import PartitionSolver, pinned_empty  # noqa: E402
+from paper_2501_05938_b200 import streamtune as st  # noqa: E402
+from paper_2501_05938_b200.solver import PM_OPT_STREAM_MODE, PM_OPT_TIMINGS  # noqa: E402
+
+SIZES = [int(k * 10**i) for i in range(3, 8) for k in (1, 2.5, 4, 5, 7.5, 8)]
+COUNTS = [1, 2, 4, 8, 16, 32]
+
+
+def synthetic(n: int, seed: int = 42):
+    """The counter-based system, generated on the device and copied to pinned
+    host buffers (the same bits as the CPU oracle's generator)."""
+    import torch
+
+    s = PartitionSolver(0)
+    arrs = s.generate_device(n, seed)
+    torch.cuda.synchronize()
+    host = []
+    for t in arrs:
+        h = pinned_empty(n)
+        h[:] = t.cpu().numpy()
+        host.append(h)
+    s.close()
+    del arrs
+    return host
+
+
+def sweep(sizes, reps: int, stream_mode: int, m: int = 10):
+    solver = PartitionSolver(0)
+    solver.set_option(PM_OPT_STREAM_MODE, stream_mode)
+    stage_rows, run_rows, raw = [], [], {}
+    for n in sizes:
+        a, b, c, d = synthetic(n)
+        x = pinned_empty(n)
+        # warm-up every count once (stream pools, allocations)
+        for ns in COUNTS:
+            solver.solve_host(a, b, c, d, m=m, num_streams=ns, out=x)
+        # StageTimings, unstreamed
+        solver.set_option(PM_OPT_TIMINGS, 1)
+        comps = []
+        for _ in range(reps):
+            solver.solve_host(a, b, c, d, m=m, num_streams=1, out=x)
+            comps.append(solver.last_stage_timings()[0])
+        solver.set_option(PM_OPT_TIMINGS, 0)
+        med = {f: statistics.median(getattr(t, f) for t in comps)
+               for f in ("t1_h2d", "t1_comp", "t1_d2h", "t2_comp", "t3_h2d", "t3_comp", "t3_d2h")}
+        stage_rows.append((n, med))
+        # T_str per count, interleaved repetitions
+        times = {ns: [] for ns in COUNTS}
+        for _ in range(reps):
+            for ns in COUNTS:
+                solver.solve_host(a, b, c, d, m=m, num_streams=ns, out=x)
+                times[ns].append(solver.last_stage_timings()[1])
+        for ns in COUNTS:
+            run_rows.append((n, ns, statistics.median(times[ns])))
+        raw[n] = {str(k): v for k, v in times.items()}
+        best = min(COUNTS, key=lambda k: statistics.median(times[k]))
+        print(f"N={n:>9d}  T_non_str={statistics.median(times[1]):9.4f} ms  "
+              f"best n={best:2d} ({statistics.median(times[best]):9.4f} ms)  "
+              f"components={ {k: round(v, 4) for k, v in med.items()} }", flush=True)
+        del a, b, c, d, x
+    solver.close()
+    return stage_rows, run_rows, raw
+
+
+def to_csv(stage_rows, run_rows):
+    s = "slae_size,t1_h2d,t1_comp,t1_d2h,t2_comp,t3_h2d,t3_comp,t3_d2h\n"
+    for n, t in stage_rows:
+        s += f"{n},{t['t1_h2d']!r},{t['t1_comp']!r},{t['t1_d2h']!r},{t['t2_comp']!r},{t['t3_h2d']!r}," \
+             f"{t['t3_comp']!r},{t['t3_d2h']!r}\n"
+    r = "slae_size,num_streams,t_str\n"
+    for n, ns, t in run_rows:
+        r += f"{n},{ns},{t!r}\n"
+    return s, r
+
+
+def validate(bundle, run_rows):
+    by = {}
+    for n, ns, t in run_rows:
+        by.setdefault(n, {})[ns] = t
+    out = []
+    for n in sorted(by):
+        meas = min(by[n], key=lambda k: by[n][k])
+        pred = st.recommend(bundle, n).chosen
+        ratio = max(pred, meas) / min(pred, meas)
+        out.append({"slae_size": n, "measured_opt": meas, "predicted": pred,
+                    "within_one_power_of_two": ratio <= 2,
+                    "t_pred_over_t_best": by[n][pred] / by[n][meas]})
+    return out
+
+
+def write_inc(bundle, path: Path, note: str):
+    path.write_text(
+        "// Generated by tools/refit.py -- the B200 re-fit of the paper's Eq. 4 / Eq. 7\n"
+        f"// ({note}).  Used by streamtune::ModelBundle::b200().\n"
+        f"b.sum_a = {bundle.sum_a!r};\nb.sum_b = {bundle.sum_b!r};\n"
+        f"b.small_a = {bundle.small_a!r};\nb.small_b = {bundle.small_b!r};\nb.small_c = {bundle.small_c!r};\n"
+        f"b.big_a = {bundle.big_a!r};\nb.big_b = {bundle.big_b!r};\nb.big_c = {bundle.big_c!r};\n"
+        f"b.size_threshold = {int(bundle.size_threshold)};\n")
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--reps", type=int, default=10)
+    p.add_argument("--out", default="refit")
+    p.add_argument("--stream-mode", type=int, default=0, help="0 pooled streams, 1 created per solve")
+    p.add_argument("--max-size", type=float, default=8e7)
+    p.add_argument("--threshold", type=int, default=1_000_000)
+    p.add_argument("--install", action="store_true")
+    args = p.parse_args()
+    out = ROOT / args.out
+    out.mkdir(parents=True, exist_ok=True)
+    sizes = [n for n in SIZES if n <= args.max_size]
+    t0 = time.time()
+    stage_rows, run_rows, raw = sweep(sizes, args.reps, args.stream_mode)
+    stage_csv, runs_csv = to_csv(stage_rows, run_rows)
+    (out / "stage_timings.csv").write_text(stage_csv)
+    (out / "streamed_runs.csv").write_text(runs_csv)
+    (out / "raw_times.json").write_text(json.dumps(raw))
+    bundle, met = st.fit_bundle(stage_csv, runs_csv, size_threshold=args.threshold, seed=42)
+    bundle.provenance.update({"fitted_on": "NVIDIA B200 (tools/refit.py, pm_solve_host_f64, m=10)",
+                              "stream_mode": "pooled" if args.stream_mode == 0 else "created per solve",
+                              "reps": args.reps, "sweep_seconds": round(time.time() - t0, 1)})
+    (out / "bundle.json").write_text(json.dumps(bundle.to_document(), indent=1))
+    val = validate(bundle, run_rows)
+    ok = sum(v["within_one_power_of_two"] for v in val)
+    exact = sum(v["predicted"] == v["measured_opt"] for v in val)
+    summary = {"sizes": len(val), "exact": exact, "within_one_power_of_two": ok,
+               "worst_t_pred_over_t_best": max(v["t_pred_over_t_best"] for v in val),
+               "metrics": met, "rows": val}
+    (out / "validation.json").write_text(json.dumps(summary, indent=1))
+    print(json.dumps({k: v for k, v in summary.items() if k != "rows"}, indent=1))
+    if args.install:
+        write_inc(bundle, ROOT / "paper_2501_05938_b200" / "csrc" / "streamtune" / "b200_bundle.inc",
+                  f"{len(val)} sizes x {len(COUNTS)} stream counts, {args.reps} reps, "
+                  f"{'pooled' if args.stream_mode == 0 else 'per-solve'} streams")
+
+
+if __name__ == "__main__":
+    main()
