@@ -38,6 +38,11 @@ constexpr int kMaxStages = 4;
 #ifndef PM_SOLVE_STAGE_ROWS
 #define PM_SOLVE_STAGE_ROWS 1
 #endif
+// ... and reads them as 16-byte pairs, recomputing the pivots in the
+// back-substitution instead of storing them (half the shared-memory traffic)
+#ifndef PM_SOLVE_PAIRS
+#define PM_SOLVE_PAIRS 1
+#endif
 constexpr int kMaxWarps = 8;  // P <= 256
 
 // ---------------------------------------------------------------------------
@@ -290,6 +295,77 @@ struct StageAcc {
   __device__ __forceinline__ void set_c(int j, double v) { sc[j] = v; }
   __device__ __forceinline__ double x(int j) const { return sb[j]; }
 };
+
+// Compile-time m, rows in the shared-memory stage, read as 16-byte pairs
+// (even m, pair-aligned rows): at stride m = 10 doubles a 16-byte access is
+// bank-conflict free where an 8-byte one is 2-way conflicted.  Within a
+// store-free stretch the compiler merges the two loads of a pair.
+template <int M>
+struct PairAcc {
+  const double* sa;
+  const double* sb;
+  const double* sc;
+  const double* sd;
+  __device__ __forceinline__ static double pick(const double* p, int j) {
+    if constexpr ((M % 2) == 0) {
+      const double2 v = *reinterpret_cast<const double2*>(p + (j & ~1));
+      return (j & 1) ? v.y : v.x;
+    } else {
+      return p[j];
+    }
+  }
+  __device__ __forceinline__ double a(int j) const { return pick(sa, j); }
+  __device__ __forceinline__ double b(int j) const { return pick(sb, j); }
+  __device__ __forceinline__ double c(int j) const { return pick(sc, j); }
+  __device__ __forceinline__ double d(int j) const { return pick(sd, j); }
+};
+
+// Stage 3 of one block straight from the stage: continuant pivots (as in
+// block_reduce_fast), forward substitution with x[s] = xs, x[e] = xe folded
+// in, back-substitution; x[0..M) returned in registers (all shared-memory
+// reads precede the caller's x stores).
+template <int M>
+__device__ __forceinline__ void block_solve_pairs(const PairAcc<M>& r, double xs, double xe,
+                                                  double (&x)[M], bool& bad) {
+  if constexpr (M == 2) {
+    x[0] = xs;
+    x[1] = xe;
+  } else {
+    constexpr int L = M - 2;
+    double q[L + 1], inv[L + 1], dp[L + 1];
+    q[0] = 1.0;
+    q[1] = r.b(1);
+    bool ok = q[1] != 0.0;
+#pragma unroll
+    for (int j = 2; j <= L; ++j) {
+      q[j] = fma(r.b(j), q[j - 1], -(r.a(j) * r.c(j - 1)) * q[j - 2]);
+      ok &= (q[j] != 0.0);
+    }
+    ok &= isfinite(q[L]) && (fabs(q[L]) > 1e-280);
+    if (ok) {
+#pragma unroll
+      for (int j = 1; j <= L; ++j) inv[j] = q[j - 1] * drcp(q[j]);
+    } else {
+      double cprev = 0.0;
+#pragma unroll
+      for (int j = 1; j <= L; ++j) {
+        const double den = (j == 1) ? r.b(1) : fma(-r.a(j), cprev, r.b(j));
+        bad |= (den == 0.0);
+        inv[j] = drcp(den);
+        cprev = r.c(j) * inv[j];
+      }
+    }
+    dp[1] = fma(-r.a(1), xs, r.d(1)) * inv[1];
+#pragma unroll
+    for (int j = 2; j <= L; ++j) dp[j] = fma(-r.a(j), dp[j - 1], r.d(j)) * inv[j];
+    dp[L] = fma(-(r.c(L) * inv[L]), xe, dp[L]);
+    x[L] = dp[L];
+#pragma unroll
+    for (int j = L - 1; j >= 1; --j) x[j] = fma(-(r.c(j) * inv[j]), x[j + 1], dp[j]);
+    x[0] = xs;
+    x[M - 1] = xe;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // CTA combine tree
@@ -810,7 +886,12 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     SmemAcc sacc{sa + r0, sb + r0, sc + r0, sd + r0, xbuf + r0};
     if constexpr (kStageRows) {
       sacc.fixup(r0, m, ctx);
+#if PM_SOLVE_PAIRS
+      const PairAcc<(M > 0 ? M : 1)> pa{sa + r0, sb + r0, sc + r0, sd + r0};
+      seg = block_reduce_fast<M, false>(pa, bad);
+#else
       seg = block_reduce_fast<M, true>(stg, bad);
+#endif
     } else if constexpr (M > 0) {
       regs.load(sa, sb, sc, sd, r0, ctx);
       __syncwarp();
@@ -861,9 +942,26 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       warp_downsweep(xf, xl, nodes, lane, nblk);
       const double* xsrc = kStageRows ? sb : xbuf;
       if constexpr (kStageRows) {
+#if PM_SOLVE_PAIRS
+        const PairAcc<(M > 0 ? M : 1)> pa{sa + r0, sb + r0, sc + r0, sd + r0};
+        double xv[(M > 0 ? M : 1)];
+        block_solve_pairs<(M > 0 ? M : 1)>(pa, xf, xl, xv, bad);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < M; ++j) bad |= !isfinite(xv[j]);
+        if constexpr ((M % 2) == 0) {
+#pragma unroll
+          for (int j = 0; j < M / 2; ++j)
+            reinterpret_cast<double2*>(sb + r0)[j] = make_double2(xv[2 * j], xv[2 * j + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < M; ++j) sb[r0 + j] = xv[j];
+        }
+#else
         block_interior_kept<M>(stg, xf, xl);
 #pragma unroll
         for (int j = 0; j < M; ++j) bad |= !isfinite(stg.x(j));
+#endif
       } else if constexpr (M > 0) {
         block_interior_kept<M>(regs, xf, xl);
 #pragma unroll
