@@ -238,7 +238,6 @@ def main():
     launches_per_step = solver.last_launch_count + (1 if world > 1 else 0)
 
     # ---- timed region: device-resident solves ---------------------------------
-    solver.set_option(PM_OPT_KERNEL_TIMES, 1)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -253,6 +252,15 @@ def main():
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    solver.check()
+    # ---- per-kernel CUDA-event times (same steps again, events bracketing every
+    # launch on its stream; kept out of the region above because events between
+    # launches would serialise the programmatic dependent launches) ----------
+    solver.set_option(PM_OPT_KERNEL_TIMES, 1)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step()
+    torch.cuda.synchronize()
     ktimes = solver.kernel_times()
     solver.set_option(PM_OPT_KERNEL_TIMES, 0)
     solver.check()

@@ -94,6 +94,8 @@ typedef struct pm_model_bundle {
 #define PM_OPT_UPPER_M 11      /* rows per thread of the warp-tile upper levels
                                   (default 0 = CTA tiles with m = 8)               */
 #define PM_OPT_ROOT_M 12       /* ROOT tile = 128 * root_m rows (default 8)        */
+#define PM_OPT_PDL 13          /* 1 (default): launch with programmatic dependent
+                                  launch (process-wide setting)                    */
 
 int pm_create(pm_handle_t* out, int device);
 int pm_destroy(pm_handle_t h);

@@ -505,6 +505,9 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       if (value < 0 || value > 4) return fail(h, PM_ERR_VALIDATION, "solve stages must lie in [0, 4]");
       h->solve_stages = (int)value;
       return PM_OK;
+    case PM_OPT_PDL:
+      pm::set_pdl(value != 0);
+      return PM_OK;
     case PM_OPT_CHAIN:
       h->opt_chain = value ? 1 : 0;
       return PM_OK;

@@ -96,6 +96,33 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// Programmatic dependent launch: let the next kernel of the stream start its
+// launch now, and wait for the previous one's results before touching them.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool g_use_pdl = true;
+
+// Launch with the programmatic-stream-serialization attribute (PDL).
+template <class K>
+static cudaError_t launch_kernel(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                                 const TileArgs& args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args);
+}
+
+void set_pdl(bool on) { g_use_pdl = on; }
 
 // ---------------------------------------------------------------------------
 // Row accessors
@@ -506,6 +533,8 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     }
   };
 
+  pdl_launch_dependents();
+  pdl_wait();
   if constexpr (BULK) {
     if (tid == 0) {
       for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -796,6 +825,8 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     fence_mbar_init();
   }
   __syncwarp();
+  pdl_launch_dependents();
+  pdl_wait();
   for (int s = 0; s < S && s < nlocal; ++s) {
     const int64_t t = next_issue_tile(s);  // all lanes advance the cursor
     if (lane == 0) issue(s, t);
@@ -1020,8 +1051,7 @@ static cudaError_t launch_warp_one(const TileArgs& args, int warps_per_cta, int 
   if (grid > need) grid = need;
   if (grid_out) *grid_out = (int)grid;
   if (grid <= 0) return cudaSuccess;
-  kern<<<(unsigned)grid, 32 * warps_per_cta, smem, st>>>(args);
-  return cudaGetLastError();
+  return launch_kernel(kern, (unsigned)grid, 32 * warps_per_cta, smem, st, args);
 }
 
 template <bool CHAIN>
@@ -1219,8 +1249,7 @@ static cudaError_t launch_one(const TileArgs& args, int P, int sm_count, cudaStr
   if (grid > ntiles) grid = ntiles;
   if (grid_out) *grid_out = (int)grid;
   if (grid <= 0) return cudaSuccess;
-  kern<<<(unsigned)grid, P, smem, st>>>(args);
-  return cudaGetLastError();
+  return launch_kernel(kern, (unsigned)grid, P, smem, st, args);
 }
 
 template <int MODE, bool BULK>

@@ -64,6 +64,8 @@ __host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages);
 cudaError_t launch_warp_tile_kernel(int mode, const TileArgs& args, int warps_per_cta,
                                     int sm_count, cudaStream_t st, int* grid_out);
 bool m_is_specialised(int m);
+// Programmatic dependent launch for the solver kernels (default on).
+void set_pdl(bool on);
 cudaError_t launch_tile_kernel(int mode, const TileArgs& args, int P, bool bulk, int sm_count,
                                cudaStream_t st, int* grid_out);
 // rows [row0, row0 + count) of the n_total-row synthetic system, stored at a[0..count)

@@ -29,6 +29,7 @@ PM_OPT_WARPS_PER_CTA = 9
 PM_OPT_CHAIN = 10
 PM_OPT_UPPER_M = 11
 PM_OPT_ROOT_M = 12
+PM_OPT_PDL = 13
 PM_MAX_M = 128
 
 
