@@ -52,13 +52,18 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=float, default=8e7, help="rows per GPU")
+    p.add_argument("--rows-per-gpu", type=float, default=8e7, help="rows per GPU (N)")
     p.add_argument("--m", type=int, default=10)
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--num-streams", type=int, default=0, help="e2e stream count (0 = predictor)")
+    p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend (tests: gloo)")
+    p.add_argument("--same-device", action="store_true",
+                   help="tests only: every rank on cuda:0 (with --dist-backend gloo)")
+    p.add_argument("--check", action="store_true",
+                   help="gather x on rank 0 and check it against the CPU oracle (small N)")
     p.add_argument("--opt", action="append", default=[],
                    help="solver option NAME=VALUE (PM_OPT_* without the prefix), experiments")
     return p.parse_args()
@@ -164,7 +169,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    n = int(args.n)
+    n = int(args.rows_per_gpu)
     cores, model = cpu_info()
     ups, threads, times = cpu_partition_baseline(n, args.m, args.seed, args.steps, args.warmup)
     line = {
@@ -201,12 +206,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.dist_backend)
 
     m = args.m
-    n_rank = int(args.n)
+    n_rank = int(args.rows_per_gpu)
     n_total = n_rank * world
     rows = split_rows(n_total, world, m)
     n_loc = rows[rank]
@@ -270,6 +280,27 @@ def main():
         ms = float(t.item())
     ms_per_step = ms / args.steps
     value = n_total * args.steps / (ms / 1e3)
+
+    check = None
+    if args.check:
+        import numpy as np
+
+        xs = x.double().cpu()
+        if world > 1:
+            mx = max(rows)
+            buf = torch.zeros(mx, dtype=torch.float64)
+            buf[:n_loc] = xs
+            parts = [torch.empty(mx, dtype=torch.float64) for _ in range(world)]
+            g = dist.new_group(backend="gloo")
+            dist.all_gather(parts, buf, group=g)
+            xs = torch.cat([p[:k] for p, k in zip(parts, rows)])
+        if rank == 0:
+            import oracle
+
+            ah, bh, ch, dh = oracle.generate(n_total, args.seed)
+            xr = oracle.thomas(ah, bh, ch, dh)
+            xn = np.ascontiguousarray(xs.numpy())
+            check = {"rel_err": oracle.rel_err(xn, xr), "residual": oracle.residual(ah, bh, ch, dh, xn)}
 
     # dominant kernel: level-0 Stage 3 (mode 1); Stage 1 (mode 0) beside it
     def avg(mode, level=0):
@@ -355,6 +386,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches_per_step * args.steps,
+            **({"check": check} if check is not None else {}),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -43,6 +43,9 @@ constexpr int kMaxStages = 4;
 #ifndef PM_SOLVE_PAIRS
 #define PM_SOLVE_PAIRS 1
 #endif
+#ifndef PM_REDUCE_PAIRS
+#define PM_REDUCE_PAIRS 0
+#endif
 constexpr int kMaxWarps = 8;  // P <= 256
 
 // ---------------------------------------------------------------------------
@@ -923,6 +926,16 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
 #else
       seg = block_reduce_fast<M, true>(stg, bad);
 #endif
+    } else if constexpr (M > 0 && MODE == kModeReduce && PM_REDUCE_PAIRS) {
+      // rows read in place as 16-byte pairs; the stage is released after the sweep
+      sacc.fixup(r0, m, ctx);
+      const PairAcc<(M > 0 ? M : 1)> pa{sa + r0, sb + r0, sc + r0, sd + r0};
+      seg = block_reduce_fast<M, false>(pa, bad);
+      __syncwarp();
+      if (k + S < nlocal) {
+        const int64_t tn = next_issue_tile(k + S);
+        if (lane == 0) issue(s, tn);
+      }
     } else if constexpr (M > 0) {
       regs.load(sa, sb, sc, sd, r0, ctx);
       __syncwarp();

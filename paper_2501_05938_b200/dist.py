@@ -51,8 +51,17 @@ class DistributedSolver:
         self.iface = torch.zeros(8, dtype=torch.float64, device=dev)
         self.iface_all = torch.zeros(8 * self.world, dtype=torch.float64, device=dev)
 
+    def _all_gather(self):
+        if self.iface.is_cuda and self.dist.get_backend(self.group) != "nccl":
+            # host-staged exchange for backends without CUDA collectives (tests)
+            h, hall = self.iface.cpu(), self.iface_all.cpu()
+            self.dist.all_gather_into_tensor(hall, h, group=self.group)
+            self.iface_all.copy_(hall)
+        else:
+            self.dist.all_gather_into_tensor(self.iface_all, self.iface, group=self.group)
+
     def solve(self, a, b, c, d, x, m: int = 10, stream=None):
         self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
-        self.dist.all_gather_into_tensor(self.iface_all, self.iface, group=self.group)
+        self._all_gather()
         self.solver.dist_solve(a, b, c, d, x, m, self.rank, self.world, self.iface_all, stream=stream)
         return x

@@ -345,3 +345,25 @@ def test_golden_scaled_systems(solver):
             x = solver.solve_device(*t, m=m)
             solver.check()
             assert oracle.rel_err(x.cpu().numpy(), xg) <= REL_TOL, (key, m)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_row_sharded_path(world, tmp_path):
+    """bench.py's multi-rank path (DistributedSolver: reduce -> all_gather ->
+    solve) with `world` processes sharing cuda:0 over gloo, checked against the
+    oracle.  (The NCCL run needs one GPU per rank.)"""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), str(root / "bench.py"),
+           "--gpus", str(world), "--steps", "3", "--warmup", "3", "--rows-per-gpu", "333337",
+           "--dist-backend", "gloo", "--same-device", "--no-e2e", "--check"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == world and line["check"]["rel_err"] <= REL_TOL
+    assert line["check"]["residual"] <= RES_TOL
