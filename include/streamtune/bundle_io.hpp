@@ -1,0 +1,75 @@
+// streamtune/bundle_io.hpp -- ModelBundle document and the table-reproduction report.
+//
+// ModelBundle serialisation: a JSON document
+// with top-level keys sum:{a,b}, overhead_small:{a,b,c}, overhead_big:{a,b,c},
+// size_threshold, candidates and optional provenance {fitted_on, seed,
+// metrics}; numbers written with 17 significant digits (round-trip exact).
+// Coefficients may be JSON numbers or numeric strings (the Python mirror
+// writes repr() strings).
+//
+// Report harness (cmd_report): regenerates Table 1, 2, 4 or
+// 5 of the paper from a bundle + the embedded ReferenceData and diffs every
+// cell against the transcription with the Acceptance-Criteria tolerances
+// (SPEC.md:545-551).  Cells that the documented reference discrepancies
+// explain (Table 4 at 8e4 with the printed
+// coefficients; Table 5 "same" rows, where the paper's own halving rule
+// disagrees with its measurement) are reported as KNOWN, not FAIL.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "streamtune/dataset.hpp"
+#include "streamtune/predictor.hpp"
+#include "streamtune/regression.hpp"
+
+namespace streamtune {
+
+struct FitMetricsDoc {  // provenance.metrics.<model>.<split>.{r_squared, mse, rmse}
+  std::map<std::string, std::map<std::string, std::map<std::string, double>>> values;
+};
+
+// cmd_fit core: Eq. 3 sums from every StageTimings row fit
+// Eq. 4; Eq. 5 overhead rows (n >= 2) split at size_threshold (inclusive on
+// the small side) fit the two Eq. 7 forms; 3:1 split with `seed`.
+// Throws TooFewObservationsError when there are no overhead observations.
+struct BundleFit {
+  ModelBundle bundle;
+  FitReport sum, small, big;
+  FitMetricsDoc metrics() const;
+};
+BundleFit fit_bundle(const StageTimingsTable& stage, const StreamedRunTable& runs,
+                     std::uint64_t size_threshold = 1000000, std::uint64_t seed = 42);
+
+// Throws ValidationError on malformed documents (missing key, non-numeric
+// coefficient, invalid candidate list).
+std::string bundle_to_document(const ModelBundle& b, const FitMetricsDoc* metrics = nullptr);
+ModelBundle bundle_from_document(const std::string& doc);
+
+enum class CellStatus { pass, fail, known };
+
+struct ReportCell {
+  std::string row;     // e.g. "N=80000" or "n=8"
+  std::string column;  // e.g. "N_pre"
+  double expected = 0.0;
+  double got = 0.0;
+  double tolerance = 0.0;
+  CellStatus status = CellStatus::pass;
+  std::string note;
+};
+
+struct TableReport {
+  std::string table;  // table1 | table2 | table4 | table5
+  std::vector<ReportCell> cells;
+  int passed = 0, failed = 0, known = 0;
+};
+
+// Throws ValidationError for an unknown table name.
+TableReport report_table(const ModelBundle& b, const std::string& table);
+
+// CSV dump of an embedded reference table (cmd dump-reference).
+std::string dump_reference(const std::string& table);
+
+}  // namespace streamtune

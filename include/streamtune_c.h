@@ -74,6 +74,31 @@ int st_derive_overhead_rows(const char* stage_csv, const char* runs_csv, uint64_
 int st_fit_bundle(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
                   uint64_t seed, pm_model_bundle* out, double* metrics, char* err, int errlen);
 
+/* simulator.  stages[7] = {stage1 h2d, comp, d2h, cpu (Stage 2),
+ * stage3 h2d, comp, d2h} in ms; n a valid stream count; out[3] = {total, stage-1
+ * makespan, stage-3 makespan}; trace (may be NULL) receives up to max_events rows of
+ * 5 doubles {engine (0 h2d, 1 comp, 2 d2h), stream, stage (1|3), start_ms, end_ms}. */
+int st_simulate(const double* stages, int n, double tau_ms, int hw_queues, double* out,
+                double* trace, int max_events, int* n_events, char* err, int errlen);
+/* holds = simulate.total >= Eq. 2 bound - 1e-9; dominance = Eq. 2 is exact */
+int st_verify_lower_bound(const double* stages, int n, double tau_ms, int* holds, int* dominance,
+                          char* err, int errlen);
+
+/* ModelBundle document: JSON, 17 significant digits.  *needed = bytes
+ * including the terminating NUL; a too-small buffer is a validation error. */
+int st_bundle_to_json(const pm_model_bundle* b, char* out, int outlen, int* needed, char* err,
+                      int errlen);
+int st_bundle_from_json(const char* doc, pm_model_bundle* out, char* err, int errlen);
+
+/* cmd_report: table in {table1, table2, table4, table5};
+ * cells: up to max_cells rows of {expected, got, tolerance, status (0 pass, 1 fail,
+ * 2 known deviation)} */
+int st_report_table(const pm_model_bundle* b, const char* table, int* passed, int* failed,
+                    int* known, double* cells, int max_cells, int* n_cells, char* err, int errlen);
+/* cmd dump-reference: CSV of an embedded paper table (table1|table2|table4|table5|tau) */
+int st_dump_reference(const char* table, char* out, int outlen, int* needed, char* err,
+                      int errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,8 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 BUILD = ROOT / "build" / "obj"
 LIB = PKG / "libpm_tridiag.so"
+CLI_SRC = PKG / "cli" / "streamtune_cli.cpp"
+CLI = PKG / "bin" / "streamtune"
 # extra nvcc flags (experiments only), e.g. PM_NVCC_FLAGS="-DPM_SOLVE_MINB=3"
 EXTRA = os.environ.get("PM_NVCC_FLAGS", "").split()
 
@@ -75,9 +77,29 @@ def build(verbose: bool = False, out: Path | None = None) -> Path:
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
         os.replace(tmp, LIB)
+    if out is None:
+        build_cli(verbose)
     if verbose:
         print(f"built {LIB}", file=sys.stderr)
     return LIB
+
+
+def build_cli(verbose: bool = False) -> Path:
+    """The `streamtune` command-line tool, a C++ executable
+    linked against libpm_tridiag.so (rpath $ORIGIN/..)."""
+    deps = [CLI_SRC, LIB] + headers()
+    if CLI.exists() and CLI.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
+        return CLI
+    CLI.parent.mkdir(parents=True, exist_ok=True)
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++17", "-O2", f"-I{INCLUDE}", str(CLI_SRC), f"-L{PKG}", "-lpm_tridiag",
+           "-Wl,-rpath,$ORIGIN/..", "-o", str(CLI)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"streamtune CLI build failed:\n{res.stdout}\n{res.stderr}")
+    if verbose:
+        print(f"built {CLI}", file=sys.stderr)
+    return CLI
 
 
 if __name__ == "__main__":

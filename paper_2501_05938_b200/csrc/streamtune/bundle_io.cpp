@@ -1,0 +1,437 @@
+// bundle_io.cpp -- ModelBundle JSON document and the table report
+// (/root/reference/SPEC.md:316, 506-515); see streamtune/bundle_io.hpp.
+#include "streamtune/bundle_io.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <charconv>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <memory>
+#include <sstream>
+
+#include "streamtune/dataset.hpp"
+
+namespace streamtune {
+
+namespace {
+
+// ---- a minimal JSON reader (objects, arrays, strings, numbers, literals) ----
+struct JVal {
+  enum Kind { null_, boolean, number, string, array, object } kind = null_;
+  double num = 0.0;
+  bool b = false;
+  std::string str;
+  std::vector<JVal> items;
+  std::vector<std::pair<std::string, JVal>> fields;
+
+  const JVal* get(const std::string& k) const {
+    for (const auto& f : fields)
+      if (f.first == k) return &f.second;
+    return nullptr;
+  }
+};
+
+class JReader {
+ public:
+  explicit JReader(const std::string& s) : s_(s) {}
+  JVal parse() {
+    JVal v = value();
+    ws();
+    if (p_ != s_.size()) fail("trailing characters");
+    return v;
+  }
+
+ private:
+  [[noreturn]] void fail(const std::string& what) const {
+    throw ValidationError("malformed model document at offset " + std::to_string(p_) + ": " + what);
+  }
+  void ws() {
+    while (p_ < s_.size() && std::isspace(static_cast<unsigned char>(s_[p_]))) ++p_;
+  }
+  char peek() {
+    ws();
+    if (p_ >= s_.size()) fail("unexpected end");
+    return s_[p_];
+  }
+  void expect(char c) {
+    if (peek() != c) fail(std::string("expected '") + c + "'");
+    ++p_;
+  }
+  std::string str() {
+    expect('"');
+    std::string out;
+    while (p_ < s_.size() && s_[p_] != '"') {
+      char c = s_[p_++];
+      if (c == '\\') {
+        if (p_ >= s_.size()) fail("bad escape");
+        const char e = s_[p_++];
+        switch (e) {
+          case 'n': out += '\n'; break;
+          case 't': out += '\t'; break;
+          case 'r': out += '\r'; break;
+          case 'b': out += '\b'; break;
+          case 'f': out += '\f'; break;
+          case 'u': {
+            if (p_ + 4 > s_.size()) fail("bad \\u escape");
+            const unsigned cp = (unsigned)std::strtoul(s_.substr(p_, 4).c_str(), nullptr, 16);
+            p_ += 4;
+            out += cp < 0x80 ? static_cast<char>(cp) : '?';
+            break;
+          }
+          default: out += e;
+        }
+      } else {
+        out += c;
+      }
+    }
+    if (p_ >= s_.size()) fail("unterminated string");
+    ++p_;
+    return out;
+  }
+  JVal value() {
+    const char c = peek();
+    JVal v;
+    if (c == '{') {
+      ++p_;
+      v.kind = JVal::object;
+      if (peek() == '}') { ++p_; return v; }
+      for (;;) {
+        std::string k = str();
+        expect(':');
+        v.fields.emplace_back(std::move(k), value());
+        if (peek() == ',') { ++p_; continue; }
+        expect('}');
+        return v;
+      }
+    }
+    if (c == '[') {
+      ++p_;
+      v.kind = JVal::array;
+      if (peek() == ']') { ++p_; return v; }
+      for (;;) {
+        v.items.push_back(value());
+        if (peek() == ',') { ++p_; continue; }
+        expect(']');
+        return v;
+      }
+    }
+    if (c == '"') {
+      v.kind = JVal::string;
+      v.str = str();
+      return v;
+    }
+    for (const char* lit : {"true", "false", "null"}) {
+      const size_t n = std::char_traits<char>::length(lit);
+      if (s_.compare(p_, n, lit) == 0) {
+        p_ += n;
+        v.kind = lit[0] == 'n' ? JVal::null_ : JVal::boolean;
+        v.b = lit[0] == 't';
+        return v;
+      }
+    }
+    const char* begin = s_.c_str() + p_;
+    char* end = nullptr;
+    v.num = std::strtod(begin, &end);
+    if (end == begin) fail("expected a value");
+    p_ += (size_t)(end - begin);
+    v.kind = JVal::number;
+    return v;
+  }
+
+  const std::string& s_;
+  size_t p_ = 0;
+};
+
+double as_number(const JVal* v, const std::string& key) {
+  if (!v) throw ValidationError("model document: missing key '" + key + "'");
+  if (v->kind == JVal::number) return v->num;
+  if (v->kind == JVal::string) {
+    char* end = nullptr;
+    const double d = std::strtod(v->str.c_str(), &end);
+    if (end != v->str.c_str() && *end == '\0') return d;
+  }
+  throw ValidationError("model document: key '" + key + "' is not a number");
+}
+
+const JVal* need_obj(const JVal& root, const std::string& key) {
+  const JVal* v = root.get(key);
+  if (!v || v->kind != JVal::object)
+    throw ValidationError("model document: missing object '" + key + "'");
+  return v;
+}
+
+std::string num17(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+
+std::string quoted(const std::string& s) {
+  std::string o = "\"";
+  for (char c : s) {
+    if (c == '"' || c == '\\') o += '\\';
+    if (c == '\n') { o += "\\n"; continue; }
+    o += c;
+  }
+  return o + "\"";
+}
+
+}  // namespace
+
+std::string bundle_to_document(const ModelBundle& b, const FitMetricsDoc* metrics) {
+  std::ostringstream o;
+  o << "{\n";
+  o << "  \"sum\": {\"a\": " << num17(b.sum_a) << ", \"b\": " << num17(b.sum_b) << "},\n";
+  o << "  \"overhead_small\": {\"a\": " << num17(b.small_a) << ", \"b\": " << num17(b.small_b)
+    << ", \"c\": " << num17(b.small_c) << "},\n";
+  o << "  \"overhead_big\": {\"a\": " << num17(b.big_a) << ", \"b\": " << num17(b.big_b)
+    << ", \"c\": " << num17(b.big_c) << "},\n";
+  o << "  \"size_threshold\": " << b.size_threshold << ",\n";
+  o << "  \"candidates\": [";
+  for (size_t k = 0; k < b.candidates.size(); ++k) o << (k ? ", " : "") << b.candidates[k].value();
+  o << "],\n";
+  o << "  \"provenance\": {\"fitted_on\": " << quoted(b.fitted_on) << ", \"seed\": " << b.seed;
+  if (metrics && !metrics->values.empty()) {
+    o << ", \"metrics\": {";
+    bool f1 = true;
+    for (const auto& m : metrics->values) {
+      o << (f1 ? "" : ", ") << quoted(m.first) << ": {";
+      f1 = false;
+      bool f2 = true;
+      for (const auto& s : m.second) {
+        o << (f2 ? "" : ", ") << quoted(s.first) << ": {";
+        f2 = false;
+        bool f3 = true;
+        for (const auto& kv : s.second) {
+          o << (f3 ? "" : ", ") << quoted(kv.first) << ": " << num17(kv.second);
+          f3 = false;
+        }
+        o << "}";
+      }
+      o << "}";
+    }
+    o << "}";
+  }
+  o << "}\n}\n";
+  return o.str();
+}
+
+ModelBundle bundle_from_document(const std::string& doc) {
+  const JVal root = JReader(doc).parse();
+  if (root.kind != JVal::object) throw ValidationError("model document: top level is not an object");
+  ModelBundle b;
+  const JVal* s = need_obj(root, "sum");
+  b.sum_a = as_number(s->get("a"), "sum.a");
+  b.sum_b = as_number(s->get("b"), "sum.b");
+  const JVal* sm = need_obj(root, "overhead_small");
+  b.small_a = as_number(sm->get("a"), "overhead_small.a");
+  b.small_b = as_number(sm->get("b"), "overhead_small.b");
+  b.small_c = as_number(sm->get("c"), "overhead_small.c");
+  const JVal* bg = need_obj(root, "overhead_big");
+  b.big_a = as_number(bg->get("a"), "overhead_big.a");
+  b.big_b = as_number(bg->get("b"), "overhead_big.b");
+  b.big_c = as_number(bg->get("c"), "overhead_big.c");
+  if (const JVal* t = root.get("size_threshold")) {
+    const double v = as_number(t, "size_threshold");
+    if (!(v >= 1.0) || v != std::floor(v)) throw ValidationError("model document: bad size_threshold");
+    b.size_threshold = static_cast<std::uint64_t>(v);
+  }
+  if (const JVal* c = root.get("candidates")) {
+    if (c->kind != JVal::array) throw ValidationError("model document: candidates is not a list");
+    b.candidates.clear();
+    for (const JVal& it : c->items) {
+      const double v = as_number(&it, "candidates[]");
+      if (v != std::floor(v)) throw ValidationError("model document: non-integer candidate");
+      b.candidates.emplace_back(static_cast<int>(v));  // throws InvalidStreamCountError
+    }
+  }
+  if (const JVal* p = root.get("provenance")) {
+    if (const JVal* f = p->get("fitted_on"))
+      if (f->kind == JVal::string) b.fitted_on = f->str;
+    if (const JVal* sd = p->get("seed"))
+      if (sd->kind == JVal::number) b.seed = static_cast<std::uint64_t>(sd->num);
+  }
+  for (double v : {b.sum_a, b.sum_b, b.small_a, b.small_b, b.small_c, b.big_a, b.big_b, b.big_c})
+    if (!std::isfinite(v)) throw ValidationError("model document: non-finite coefficient");
+  b.validate();
+  return b;
+}
+
+BundleFit fit_bundle(const StageTimingsTable& stage, const StreamedRunTable& runs,
+                     std::uint64_t size_threshold, std::uint64_t seed) {
+  SplitConfig cfg;
+  cfg.seed = seed;
+  std::vector<std::pair<std::uint64_t, double>> sum_rows;
+  for (const StageTimings& t : stage.rows) sum_rows.emplace_back(t.slae_size, overlap_sum(t));
+  std::vector<OverheadRow> ovh = derive_overhead_rows(stage, runs), small, big;
+  for (const OverheadRow& r : ovh) (r.slae_size <= size_threshold ? small : big).push_back(r);
+  if (ovh.empty()) throw TooFewObservationsError("no overhead observations (only n = 1 runs)");
+  BundleFit f;
+  f.sum = fit_sum_model(sum_rows, cfg);
+  f.small = fit_overhead_small(small, cfg);
+  f.big = fit_overhead_big(big, cfg);
+  ModelBundle& b = f.bundle;
+  b.sum_a = f.sum.coefficients[0];
+  b.sum_b = f.sum.coefficients[1];
+  b.small_a = f.small.coefficients[0];
+  b.small_b = f.small.coefficients[1];
+  b.small_c = f.small.coefficients[2];
+  b.big_a = f.big.coefficients[0];
+  b.big_b = f.big.coefficients[1];
+  b.big_c = f.big.coefficients[2];
+  b.size_threshold = size_threshold;
+  b.seed = seed;
+  b.validate();
+  return f;
+}
+
+FitMetricsDoc BundleFit::metrics() const {
+  FitMetricsDoc d;
+  const std::pair<const char*, const FitReport*> reps[3] = {{"sum", &sum}, {"small", &small}, {"big", &big}};
+  for (const auto& r : reps) {
+    const std::pair<const char*, const Metrics*> sp[2] = {{"train", &r.second->train},
+                                                          {"test", &r.second->test}};
+    for (const auto& s : sp)
+      d.values[r.first][s.first] = {{"r_squared", s.second->r_squared}, {"mse", s.second->mse},
+                                    {"rmse", s.second->rmse}};
+  }
+  return d;
+}
+
+// ---- report harness ---------------------------------------------------------------
+
+namespace {
+
+std::string size_label(std::uint64_t n) { return "N=" + std::to_string(n); }
+
+void add(TableReport& r, ReportCell c) {
+  if (c.status == CellStatus::pass) {
+    const bool ok = std::fabs(c.got - c.expected) <= c.tolerance;
+    if (!ok) c.status = CellStatus::fail;
+  }
+  (c.status == CellStatus::pass ? r.passed : c.status == CellStatus::fail ? r.failed : r.known)++;
+  r.cells.push_back(std::move(c));
+}
+
+}  // namespace
+
+TableReport report_table(const ModelBundle& b, const std::string& table) {
+  TableReport r;
+  r.table = table;
+  const double tau = ReferenceData::tau_ms;
+  if (table == "table1") {
+    // Eq. 3 sums and the Gomez-Luna optimum (criterion 2)
+    for (const auto& t : ReferenceData::table1()) {
+      StageTimings s;
+      s.slae_size = t.size;
+      s.t1_comp = t.t1_comp;
+      s.t1_d2h = t.t1_d2h;
+      s.t3_h2d = t.t3_h2d;
+      s.t3_comp = t.t3_comp;
+      add(r, {size_label(t.size), "sum", t.sum, overlap_sum(s), 1e-6});
+      add(r, {size_label(t.size), "gomez_luna", t.gomez_luna, gomez_luna_optimum(t.sum, tau), 0.05});
+    }
+  } else if (table == "table2") {
+    // Eq. 5 / Eq. 6 columns and the highlighted optimum (criterion 3)
+    int best_n = 0;
+    double best = -1e300;
+    for (const auto& t : ReferenceData::table2()) {
+      const StreamCount n(t.n);
+      const std::string row = "n=" + std::to_string(t.n);
+      const double ovh = overhead_from_measurement(t.t_str, t.t_non_str, n, t.sum);
+      const double ben = overlap_benefit(n, t.sum, ovh);
+      add(r, {row, "T_overhead", t.overhead, ovh, 1e-6});
+      add(r, {row, "benefit", t.benefit, ben, 1e-6});
+      if (ben > best) { best = ben; best_n = t.n; }
+    }
+    add(r, {"argmax", "num_str", 8.0, (double)best_n, 0.0});
+  } else if (table == "table4") {
+    // N_pre column (criterion 1)
+    for (const auto& t : ReferenceData::table4()) {
+      const int got = recommend(b, t.size).chosen.value();
+      ReportCell c{size_label(t.size), "N_pre", (double)t.n_pre, (double)got, 0.0};
+      if (got != t.n_pre && t.size == 80000 && got == 2) {
+        c.status = CellStatus::known;
+        c.note = "printed Eq. 4/7 coefficients give benefit(2) = +0.0227 ms (SURVEY.md App. B.1)";
+      }
+      add(r, c);
+    }
+  } else if (table == "table5") {
+    // FP32 halving rule (criterion 6).  Column "rule": the halving rule applied
+    // to Table 5's own FP64 column (bundle-independent) on the rows marked
+    // "half".  Column "fp32": recommend_fp32 with the bundle; where the
+    // bundle's FP64 choice differs from Table 5's FP64 column (Table 4's
+    // deliberate mismatches) the cell cannot match and is KNOWN.
+    for (const auto& t : ReferenceData::table5()) {
+      const std::uint64_t n = t.size ? t.size : 100000;
+      const std::string row = t.size ? size_label(t.size) : std::string("N<=1e5");
+      const char* same = "Table 5 row marked 'same': the paper's halving rule deviates from its measurement";
+      ReportCell rule{row, "rule", (double)t.fp32, (double)std::max(1, t.fp64 / 2), 0.0};
+      if (!t.half && t.fp32 != std::max(1, t.fp64 / 2)) {
+        rule.status = CellStatus::known;
+        rule.note = same;
+      }
+      add(r, rule);
+      const int fp64 = recommend(b, n).chosen.value();
+      const int got = recommend_fp32(b, n).value();
+      ReportCell c{row, "fp32", (double)t.fp32, (double)got, 0.0};
+      if (got != t.fp32) {
+        if (!t.half) {
+          c.status = CellStatus::known;
+          c.note = same;
+        } else if (fp64 != t.fp64) {
+          c.status = CellStatus::known;
+          c.note = "bundle's FP64 choice " + std::to_string(fp64) + " differs from Table 5's FP64 column " +
+                   std::to_string(t.fp64);
+        }
+      }
+      add(r, c);
+    }
+  } else {
+    throw ValidationError("unknown reference table '" + table + "' (table1|table2|table4|table5)");
+  }
+  return r;
+}
+
+namespace {
+struct Short {  // shortest representation that round-trips
+  double v;
+};
+std::ostream& operator<<(std::ostream& o, Short s) {
+  char buf[64];
+  auto res = std::to_chars(buf, buf + sizeof(buf), s.v);
+  return o.write(buf, res.ptr - buf);
+}
+}  // namespace
+
+std::string dump_reference(const std::string& table) {
+  std::ostringstream o;
+  if (table == "table1") {
+    o << "slae_size,t1_comp,t1_d2h,t3_h2d,t3_comp,sum,gomez_luna,actual\n";
+    for (const auto& t : ReferenceData::table1())
+      o << t.size << ',' << Short{t.t1_comp} << ',' << Short{t.t1_d2h} << ',' << Short{t.t3_h2d} << ',' << Short{t.t3_comp} << ','
+        << Short{t.sum} << ',' << Short{t.gomez_luna} << ',' << t.actual << '\n';
+  } else if (table == "table2") {
+    o << "num_streams,t_str,t_non_str,sum,overhead,benefit\n";
+    for (const auto& t : ReferenceData::table2())
+      o << t.n << ',' << Short{t.t_str} << ',' << Short{t.t_non_str} << ',' << Short{t.sum} << ',' << Short{t.overhead} << ','
+        << Short{t.benefit} << '\n';
+  } else if (table == "table4") {
+    o << "slae_size,n_actual,n_predicted\n";
+    for (const auto& t : ReferenceData::table4()) o << t.size << ',' << t.n_act << ',' << t.n_pre << '\n';
+  } else if (table == "table5") {
+    o << "slae_size,fp32,fp64,comparison\n";
+    for (const auto& t : ReferenceData::table5())
+      o << (t.size ? std::to_string(t.size) : std::string("<=100000")) << ',' << t.fp32 << ','
+        << t.fp64 << ',' << (t.half ? "half" : "same") << '\n';
+  } else if (table == "tau") {
+    o << "tau_ms\n" << Short{ReferenceData::tau_ms} << '\n';
+  } else {
+    throw ValidationError("unknown reference table '" + table + "' (table1|table2|table4|table5|tau)");
+  }
+  return o.str();
+}
+
+}  // namespace streamtune

@@ -1,15 +1,18 @@
 // st_capi.cpp -- extern "C" wrappers of the streamtune C++ API (include/streamtune_c.h).
 #include "streamtune_c.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <sstream>
 #include <string>
 #include <vector>
 
+#include "streamtune/bundle_io.hpp"
 #include "streamtune/dataset.hpp"
 #include "streamtune/predictor.hpp"
 #include "streamtune/regression.hpp"
+#include "streamtune/simulator.hpp"
 #include "streamtune/timing_model.hpp"
 
 namespace {
@@ -257,37 +260,26 @@ int st_derive_overhead_rows(const char* stage_csv, const char* runs_csv, uint64_
   });
 }
 
+void bundle_to_c(const ModelBundle& b, pm_model_bundle* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->sum_a = b.sum_a; out->sum_b = b.sum_b;
+  out->small_a = b.small_a; out->small_b = b.small_b; out->small_c = b.small_c;
+  out->big_a = b.big_a; out->big_b = b.big_b; out->big_c = b.big_c;
+  out->size_threshold = b.size_threshold;
+  out->num_candidates = (int32_t)std::min<size_t>(b.candidates.size(), 5);
+  for (int k = 0; k < out->num_candidates; ++k) out->candidates[k] = b.candidates[k].value();
+}
+
 int st_fit_bundle(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
                   uint64_t seed, pm_model_bundle* out, double* met, char* err, int errlen) {
   return guarded(err, errlen, [&] {
     std::istringstream s1(stage_csv ? stage_csv : ""), s2(runs_csv ? runs_csv : "");
     StageTimingsTable st = load_stage_timings(s1);
     StreamedRunTable rt = load_streamed_runs(s2);
-    SplitConfig cfg;
-    cfg.seed = seed;
-    std::vector<std::pair<uint64_t, double>> sum_rows;
-    for (const StageTimings& t : st.rows) sum_rows.emplace_back(t.slae_size, overlap_sum(t));
-    std::vector<OverheadRow> ovh = derive_overhead_rows(st, rt), small, big;
-    for (const OverheadRow& r : ovh) (r.slae_size <= size_threshold ? small : big).push_back(r);
-    if (ovh.empty()) throw TooFewObservationsError("no overhead observations (only n = 1 runs)");
-    FitReport fs = fit_sum_model(sum_rows, cfg);
-    FitReport fsm = fit_overhead_small(small, cfg);
-    FitReport fbg = fit_overhead_big(big, cfg);
-    ModelBundle b;
-    b.sum_a = fs.coefficients[0]; b.sum_b = fs.coefficients[1];
-    b.small_a = fsm.coefficients[0]; b.small_b = fsm.coefficients[1]; b.small_c = fsm.coefficients[2];
-    b.big_a = fbg.coefficients[0]; b.big_b = fbg.coefficients[1]; b.big_c = fbg.coefficients[2];
-    b.size_threshold = size_threshold;
-    b.validate();
-    std::memset(out, 0, sizeof(*out));
-    out->sum_a = b.sum_a; out->sum_b = b.sum_b;
-    out->small_a = b.small_a; out->small_b = b.small_b; out->small_c = b.small_c;
-    out->big_a = b.big_a; out->big_b = b.big_b; out->big_c = b.big_c;
-    out->size_threshold = b.size_threshold;
-    out->num_candidates = 5;
-    for (int k = 0; k < 5; ++k) out->candidates[k] = 2 << k;
+    BundleFit f = fit_bundle(st, rt, size_threshold, seed);
+    bundle_to_c(f.bundle, out);
     if (met) {
-      const FitReport* reps[3] = {&fs, &fsm, &fbg};
+      const FitReport* reps[3] = {&f.sum, &f.small, &f.big};
       for (int r = 0; r < 3; ++r) {
         const Metrics* ms[2] = {&reps[r]->train, &reps[r]->test};
         for (int s = 0; s < 2; ++s) {
@@ -297,6 +289,99 @@ int st_fit_bundle(const char* stage_csv, const char* runs_csv, uint64_t size_thr
         }
       }
     }
+  });
+}
+
+static PipelineSpec spec_from_c(const double* stages, int n, double tau_ms, int hw_queues) {
+  if (!stages) throw ValidationError("null stage durations");
+  PipelineSpec p;
+  p.stage1 = StageSpec{stages[0], stages[1], stages[2]};
+  p.cpu_ms = stages[3];
+  p.stage3 = StageSpec{stages[4], stages[5], stages[6]};
+  p.num_streams = StreamCount(n);
+  p.tau_ms = tau_ms;
+  p.hw_queues = hw_queues;
+  return p;
+}
+
+int st_simulate(const double* stages, int n, double tau_ms, int hw_queues, double* out,
+                double* trace, int max_events, int* n_events, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    SimResult r = simulate(spec_from_c(stages, n, tau_ms, hw_queues));
+    if (out) {
+      out[0] = r.total_ms;
+      out[1] = r.stage1_makespan_ms;
+      out[2] = r.stage3_makespan_ms;
+    }
+    if (n_events) *n_events = (int)r.trace.size();
+    if (trace)
+      for (int k = 0; k < (int)r.trace.size() && k < max_events; ++k) {
+        const TraceEvent& e = r.trace[k];
+        double* row = trace + 5 * (size_t)k;
+        row[0] = (double)static_cast<int>(e.engine);
+        row[1] = e.stream;
+        row[2] = e.stage;
+        row[3] = e.start_ms;
+        row[4] = e.end_ms;
+      }
+  });
+}
+
+int st_verify_lower_bound(const double* stages, int n, double tau_ms, int* holds, int* dominance,
+                          char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    const PipelineSpec p = spec_from_c(stages, n, tau_ms, 32);
+    if (holds) *holds = verify_lower_bound(p) ? 1 : 0;
+    if (dominance) *dominance = dominance_holds(p) ? 1 : 0;
+  });
+}
+
+static int copy_out(const std::string& s, char* out, int outlen, int* needed) {
+  if (needed) *needed = (int)s.size() + 1;
+  if (!out || outlen < (int)s.size() + 1) return 0;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 1;
+}
+
+int st_bundle_to_json(const pm_model_bundle* b, char* out, int outlen, int* needed, char* err,
+                      int errlen) {
+  return guarded(err, errlen, [&] {
+    if (!copy_out(bundle_to_document(bundle_from_c(b)), out, outlen, needed))
+      throw ValidationError("output buffer too small");
+  });
+}
+
+int st_bundle_from_json(const char* doc, pm_model_bundle* out, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    if (!doc || !out) throw ValidationError("null argument");
+    bundle_to_c(bundle_from_document(doc), out);
+  });
+}
+
+int st_report_table(const pm_model_bundle* b, const char* table, int* passed, int* failed,
+                    int* known, double* cells, int max_cells, int* n_cells, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    TableReport r = report_table(bundle_from_c(b), table ? table : "");
+    if (passed) *passed = r.passed;
+    if (failed) *failed = r.failed;
+    if (known) *known = r.known;
+    if (n_cells) *n_cells = (int)r.cells.size();
+    if (cells)
+      for (int k = 0; k < (int)r.cells.size() && k < max_cells; ++k) {
+        double* row = cells + 4 * (size_t)k;
+        row[0] = r.cells[k].expected;
+        row[1] = r.cells[k].got;
+        row[2] = r.cells[k].tolerance;
+        row[3] = (double)static_cast<int>(r.cells[k].status);
+      }
+  });
+}
+
+int st_dump_reference(const char* table, char* out, int outlen, int* needed, char* err,
+                      int errlen) {
+  return guarded(err, errlen, [&] {
+    if (!copy_out(dump_reference(table ? table : ""), out, outlen, needed))
+      throw ValidationError("output buffer too small");
   });
 }
 

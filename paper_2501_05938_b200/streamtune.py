@@ -274,3 +274,90 @@ def fit_bundle(stage_csv: str, runs_csv: str, size_threshold: int = 1_000_000, s
         m[model] = {"train": dict(zip(names, list(met)[6 * i: 6 * i + 3])),
                     "test": dict(zip(names, list(met)[6 * i + 3: 6 * i + 6]))}
     return ModelBundle.from_c(b, provenance={"seed": seed, "metrics": m}), m
+
+
+# ---- simulator -----------------------------------------------------
+ENGINES = ("h2d", "comp", "d2h")
+
+
+@dataclass
+class PipelineSpec:
+    """streamtune::PipelineSpec: per-stage (h2d, comp, d2h) ms, the CPU Stage 2, n, tau."""
+    stage1: tuple = (0.0, 0.0, 0.0)
+    cpu_ms: float = 0.0
+    stage3: tuple = (0.0, 0.0, 0.0)
+    num_streams: int = 1
+    tau_ms: float = 0.0
+    hw_queues: int = 32
+
+    def _stages(self):
+        return (C.c_double * 7)(*[float(v) for v in (*self.stage1, self.cpu_ms, *self.stage3)])
+
+    def timings(self, slae_size: int = 1) -> StageTimings:
+        return StageTimings(slae_size, *self.stage1, self.cpu_ms, *self.stage3)
+
+
+@dataclass
+class SimResult:
+    total_ms: float
+    stage1_makespan_ms: float
+    stage3_makespan_ms: float
+    trace: list  # (engine, stream, stage, start_ms, end_ms)
+
+
+def simulate(spec: PipelineSpec, trace: bool = True) -> SimResult:
+    out = (C.c_double * 3)()
+    cap = 6 * max(1, int(spec.num_streams)) if trace else 0
+    tr = (C.c_double * max(1, 5 * cap))()
+    ne = C.c_int()
+    _call(_lib.load().st_simulate, spec._stages(), int(spec.num_streams), float(spec.tau_ms),
+          int(spec.hw_queues), out, tr if trace else None, cap, C.byref(ne))
+    events = []
+    for k in range(min(ne.value, cap)):
+        e, s, g, t0, t1 = tr[5 * k: 5 * k + 5]
+        events.append((ENGINES[int(e)], int(s), int(g), t0, t1))
+    return SimResult(out[0], out[1], out[2], events)
+
+
+def verify_lower_bound(spec: PipelineSpec) -> tuple[bool, bool]:
+    """(simulate.total >= Eq. 2 bound - 1e-9, dominance regime holds)."""
+    h, d = C.c_int(), C.c_int()
+    _call(_lib.load().st_verify_lower_bound, spec._stages(), int(spec.num_streams), float(spec.tau_ms),
+          C.byref(h), C.byref(d))
+    return bool(h.value), bool(d.value)
+
+
+# ---- bundle document / report harness (SPEC.md:316, 506-515) -----------------------------
+def bundle_to_json(bundle: ModelBundle) -> str:
+    b = bundle.to_c()
+    need = C.c_int()
+    buf = C.create_string_buffer(4096)
+    _call(_lib.load().st_bundle_to_json, C.byref(b), buf, len(buf), C.byref(need))
+    return buf.value.decode()
+
+
+def bundle_from_json(doc: str) -> ModelBundle:
+    b = ModelBundleC()
+    _call(_lib.load().st_bundle_from_json, doc.encode(), C.byref(b))
+    return ModelBundle.from_c(b)
+
+
+STATUS = ("PASS", "FAIL", "KNOWN")
+
+
+def report_table(bundle: ModelBundle, table: str) -> dict:
+    b = bundle.to_c()
+    p, f, k, nc = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    cells = (C.c_double * (4 * 64))()
+    _call(_lib.load().st_report_table, C.byref(b), table.encode(), C.byref(p), C.byref(f), C.byref(k),
+          cells, 64, C.byref(nc))
+    rows = [(cells[4 * i], cells[4 * i + 1], cells[4 * i + 2], STATUS[int(cells[4 * i + 3])])
+            for i in range(min(nc.value, 64))]
+    return {"passed": p.value, "failed": f.value, "known": k.value, "cells": rows}
+
+
+def dump_reference(table: str) -> str:
+    need = C.c_int()
+    buf = C.create_string_buffer(8192)
+    _call(_lib.load().st_dump_reference, table.encode(), buf, len(buf), C.byref(need))
+    return buf.value.decode()
