@@ -52,6 +52,11 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="single", choices=["single", "batch"],
+                   help="single: config 3/5 (one system, row-sharded for N>1); "
+                        "batch: config 4 (--batch systems of --batch-rows, split over the ranks)")
+    p.add_argument("--batch", type=int, default=4096)
+    p.add_argument("--batch-rows", type=int, default=100_000)
     p.add_argument("--rows-per-gpu", type=float, default=8e7, help="rows per GPU (N)")
     p.add_argument("--m", type=int, default=10)
     p.add_argument("--seed", type=int, default=42)
@@ -189,6 +194,126 @@ def run_reference(args):
     return 0
 
 
+def run_batch(args, world, rank, local):
+    """BASELINE config 4: `--batch` independent systems of `--batch-rows` rows,
+    split contiguously over the ranks with no collective (strong scaling: the
+    total batch is fixed).  One step = one pm_solve_batch_device_f64 call on
+    this rank's systems (the cluster-per-system kernel: 40 algorithmic B per
+    unknown, the Stage-3 re-read served from L2)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.solver import PM_OPT_KERNEL_TIMES
+
+    nps, m = args.batch_rows, args.m
+    counts = [args.batch // world + (1 if r < args.batch % world else 0) for r in range(world)]
+    nb = counts[rank]
+    n_loc = nb * nps
+    solver = PartitionSolver(local)
+    import paper_2501_05938_b200.solver as _solver_mod
+    for kv in args.opt:
+        name, val = kv.split("=")
+        solver.set_option(getattr(_solver_mod, "PM_OPT_" + name.upper()), int(val))
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    first = sum(counts[:rank])
+    with torch.cuda.stream(stream):
+        # system k of the batch = rows [k*nps, (k+1)*nps) of one long synthetic stream
+        a, b, c, d = solver.generate_range_device(args.batch * nps, first * nps, n_loc, args.seed, stream=sh)
+        x = torch.empty(n_loc, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+
+    def step():
+        solver.solve_batch_device(a, b, c, d, n_per_system=nps, m=m, out=x, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    solver.check()
+    plan = solver.last_batch_plan()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step()
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    solver.check()
+    solver.set_option(PM_OPT_KERNEL_TIMES, 1)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step()
+    torch.cuda.synchronize()
+    kt = solver.kernel_times()
+    solver.set_option(PM_OPT_KERNEL_TIMES, 0)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    n_total = args.batch * nps
+    value = n_total * args.steps / (ms / 1e3)
+    peak, peak_src = peaks()
+    if plan["cluster"]:
+        # one launch per step: the cluster kernel, 40 algorithmic B/unknown
+        bpu = 40.0
+        kms = sum(t for (md, _, t) in kt if md == 4) / max(1, sum(1 for (md, _, _) in kt if md == 4))
+        kname = ("batch_cluster_kernel: 40 B/unknown (a,b,c,d read once from HBM, x written; "
+                 "Stage-3 re-read from L2)")
+        ach = bpu * n_loc / (kms / 1e3) / 1e9
+    else:
+        # level kernels over the batch as one long system: dominant kernel =
+        # level-0 Stage 3 (40 B/unknown); the whole step moves 72 B/unknown
+        bpu = 72.0
+        v = [t for (md, lv, t) in kt if md == 1 and lv == 0]
+        kms = sum(v) / max(1, len(v))
+        kname = "Stage 3 (SOLVE level 0): 40 B/unknown; whole step 72 B/unknown"
+        ach = 40.0 * n_loc / (kms / 1e3) / 1e9
+    whole = bpu * n_loc / (ms_per_step / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists() and nps == 100_000 and args.batch == 4096 and world == 1:
+        try:
+            traffic = json.loads(tf.read_text()).get(
+                "batch_cluster_bytes_per_launch" if plan["cluster"] else "batch_solve_level0_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter-based generator, seed %d)" % args.seed,
+            "config": {"workload": f"batch of {args.batch} independent FP64 SLAEs, N={nps} each, m={m} "
+                                   "(BASELINE config 4), systems split over the ranks",
+                       "batch": args.batch, "n_per_system": nps, "m": m, "systems_per_gpu": counts,
+                       "parallelism": f"batch-sharded x{world}" if world > 1 else "single GPU",
+                       "cluster_plan": plan,
+                       "l2": "inputs %.1f GB/GPU > 126 MB L2 (no flush needed)" % (32 * n_loc / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "traffic": traffic, "kernel": kname, "peak_source": peak_src, "kernel_ms": kms,
+                         "whole_step": {"achieved": whole, "frac": whole / peak, "bytes_per_unknown": bpu}},
+            "e2e": None,
+            "cpu_baseline": None,
+            "gpu_launches": args.steps * (1 if plan["cluster"] else 5),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    solver.close()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -215,6 +340,8 @@ def main():
         else:
             dist.init_process_group(args.dist_backend)
 
+    if args.workload == "batch":
+        return run_batch(args, world, rank, local)
     m = args.m
     n_rank = int(args.rows_per_gpu)
     n_total = n_rank * world
@@ -281,11 +408,11 @@ def main():
     ms_per_step = ms / args.steps
     value = n_total * args.steps / (ms / 1e3)
 
-    check = None
-    if args.check:
+    def gather_check(x_local):
+        """Gather the ranks' rows on rank 0 and check them against the oracle."""
         import numpy as np
 
-        xs = x.double().cpu()
+        xs = x_local.double().cpu()
         if world > 1:
             mx = max(rows)
             buf = torch.zeros(mx, dtype=torch.float64)
@@ -294,13 +421,16 @@ def main():
             g = dist.new_group(backend="gloo")
             dist.all_gather(parts, buf, group=g)
             xs = torch.cat([p[:k] for p, k in zip(parts, rows)])
-        if rank == 0:
-            import oracle
+        if rank != 0:
+            return None
+        import oracle
 
-            ah, bh, ch, dh = oracle.generate(n_total, args.seed)
-            xr = oracle.thomas(ah, bh, ch, dh)
-            xn = np.ascontiguousarray(xs.numpy())
-            check = {"rel_err": oracle.rel_err(xn, xr), "residual": oracle.residual(ah, bh, ch, dh, xn)}
+        ah, bh, ch, dh = oracle.generate(n_total, args.seed)
+        xr = oracle.thomas(ah, bh, ch, dh)
+        xn = np.ascontiguousarray(xs.numpy())
+        return {"rel_err": oracle.rel_err(xn, xr), "residual": oracle.residual(ah, bh, ch, dh, xn)}
+
+    check = gather_check(x) if args.check else None
 
     # dominant kernel: level-0 Stage 3 (mode 1); Stage 1 (mode 0) beside it
     def avg(mode, level=0):
@@ -324,33 +454,53 @@ def main():
         except (OSError, ValueError):
             traffic = None
 
-    # ---- e2e through the public host API (N = 1; ranks > 1 skip) --------------
+    # ---- e2e through the public host API: pinned host rows in, x out --------
+    # N = 1: pm_solve_host_f64 (chunked H2D -> Stage 1 per stream, upper
+    # levels, Stage 3 -> D2H per stream; stream count from the predictor).
+    # N > 1: DistributedSolver.solve_host on every rank (H2D of the rank's
+    # rows, row-sharded solve with the NCCL all-gather, D2H), max over ranks.
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
+        host = [pinned_empty(n_loc) for _ in range(5)]
+        for hbuf, t in zip(host, (a, b, c, d)):
+            torch.from_numpy(hbuf).copy_(t)  # the same synthetic rows, staged once
         del a, b, c, d
         torch.cuda.empty_cache()
-        host = [pinned_empty(n_loc) for _ in range(5)]
-        import oracle  # generator only (bit-identical inputs); not the timed path
-
-        ah, bh, ch, dh = oracle.generate(n_loc, args.seed)
-        for hbuf, v in zip(host, (ah, bh, ch, dh)):
-            hbuf[:] = v
-        del ah, bh, ch, dh
         xs = host[4]
         ns = args.num_streams
+        used = 1
+        if world == 1:
+            def e2e_step():
+                solver.solve_host(*host[:4], m=m, num_streams=ns, out=xs)
+        else:
+            def e2e_step():
+                dsolver.solve_host(*host[:4], xs, m=m, stream=stream)
         for _ in range(2):
-            solver.solve_host(*host[:4], m=m, num_streams=ns, out=xs)
+            e2e_step()
         times = []
         for _ in range(args.e2e_steps):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            solver.solve_host(*host[:4], m=m, num_streams=ns, out=xs)
+            e2e_step()
             times.append(time.perf_counter() - t0)
-            _, _, used = solver.last_stage_timings()
+            if world == 1:
+                _, _, used = solver.last_stage_timings()
         t_e2e = statistics.median(times)
-        e2e = {"value": n_loc / t_e2e, "unit": "unknowns/s", "h2d_bytes_per_step": 32 * n_loc,
-               "d2h_bytes_per_step": 8 * n_loc, "ms_per_step": t_e2e * 1e3, "num_streams": used,
-               "link_gbs": 40 * n_loc / t_e2e / 1e9, "steps": args.e2e_steps,
-               "timing": "host wall clock around pm_solve_host_f64, median"}
+        if world > 1:
+            t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        e2e = {"value": n_total / t_e2e, "unit": "unknowns/s", "h2d_bytes_per_step": 32 * n_total,
+               "d2h_bytes_per_step": 8 * n_total, "ms_per_step": t_e2e * 1e3,
+               "num_streams": used if world == 1 else None,
+               "link_gbs_per_gpu": 40 * n_loc / t_e2e / 1e9, "steps": args.e2e_steps,
+               "timing": ("host wall clock around pm_solve_host_f64, median" if world == 1 else
+                          "host wall clock around DistributedSolver.solve_host per rank, median, max over ranks")}
+        if args.check:
+            ce = gather_check(torch.from_numpy(xs))
+            if check is not None and ce is not None:
+                check["e2e"] = ce
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -96,6 +96,19 @@ typedef struct pm_model_bundle {
 #define PM_OPT_ROOT_M 12       /* ROOT tile = 128 * root_m rows (default 8)        */
 #define PM_OPT_PDL 13          /* 1 (default): launch with programmatic dependent
                                   launch (process-wide setting)                    */
+#define PM_OPT_BATCH_CLUSTER 14 /* 1: pm_solve_batch_device_f64 runs one thread-
+                                  block cluster per system (all stages while the
+                                  system is L2-resident: 40 B/unknown of HBM
+                                  traffic) when it applies: m in {2, 8, 10, 16},
+                                  even n_per_system > 32*m, 16-byte aligned arrays,
+                                  the CTA's tile trees fit shared memory.
+                                  0 (default): one long system through the level
+                                  kernels (72 B/unknown, faster on B200 today:
+                                  DESIGN.md §6)                                   */
+#define PM_OPT_BATCH_L2_MB 15  /* L2 budget for the systems in flight (default 64) */
+#define PM_OPT_BATCH_CLUSTER_SIZE 16 /* force CTAs per cluster, 1..8 (0 = plan)   */
+#define PM_OPT_BATCH_WARPS 17  /* force warps per CTA, 4..16 (0 = plan)           */
+#define PM_OPT_BATCH_STAGES 18 /* force bulk-copy stages per warp, 1..2 (0 = plan) */
 
 int pm_create(pm_handle_t* out, int device);
 int pm_destroy(pm_handle_t h);
@@ -110,10 +123,16 @@ int pm_solve_device_f64(pm_handle_t h, const double* a, const double* b, const d
 
 /* Batch of independent systems stored back to back (system k occupies rows
  * [k*n_per_system, (k+1)*n_per_system)); each system's first a and last c
- * are ignored.  Asynchronous like pm_solve_device_f64. */
+ * are ignored.  Asynchronous like pm_solve_device_f64.  See
+ * PM_OPT_BATCH_CLUSTER for the cluster-per-system kernel. */
 int pm_solve_batch_device_f64(pm_handle_t h, const double* a, const double* b, const double* c,
                               const double* d, double* x, int64_t n_per_system, int64_t batch,
                               int32_t m, void* stream);
+
+/* Configuration of the last batch solve's cluster kernel: {CTAs per cluster,
+ * warps per CTA, stages, max tiles per CTA, tiles per system, clusters}; all
+ * zero when the last batch solve used the level kernels. */
+int pm_last_batch_plan(pm_handle_t h, int32_t* out6);
 
 /* Waits for the handle's last stream; PM_ERR_COMPUTATION if any solve since
  * the previous check met a zero or non-finite pivot (the flag is cleared). */

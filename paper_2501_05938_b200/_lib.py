@@ -62,6 +62,7 @@ PM_SIGNATURES = [
     ("pm_kernel_times", C.c_int,
      [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int32]),
     ("pm_last_plan", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]),
+    ("pm_last_batch_plan", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     # streamtune_c.h
     ("st_stream_count_is_valid", C.c_int, [C.c_int]),
     ("st_validate_stage_timings", C.c_int, [C.POINTER(StageTimingsC)] + _ERR),

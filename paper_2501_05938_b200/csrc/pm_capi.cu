@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "pm_batch.h"
 #include "pm_kernels.h"
 #include "pm_tridiag.h"
 #include "streamtune/predictor.hpp"
@@ -74,6 +75,13 @@ struct pm_handle_s {
   int warp_tiles = 1;
   int solve_stages = 1;   // level-0 Stage 3 ring depth (0 = same as `stages`)
   int warps_per_cta = 4;
+  // batch cluster kernel
+  int batch_cluster = 0;
+  int batch_l2_mb = 64;
+  int batch_force_cluster = 0;
+  int batch_force_warps = 0;
+  int batch_force_stages = 0;
+  pm::BatchPlan last_batch_plan{0, 0, 0, 0, 0, 0};
   // device scratch for upper levels (+ dist boundary values)
   double* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -524,6 +532,26 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       if (value < 1 || value > 8) return fail(h, PM_ERR_VALIDATION, "warps per CTA must lie in [1, 8]");
       h->warps_per_cta = (int)value;
       return PM_OK;
+    case PM_OPT_BATCH_CLUSTER:
+      h->batch_cluster = value ? 1 : 0;
+      return PM_OK;
+    case PM_OPT_BATCH_L2_MB:
+      if (value < 1 || value > 1024) return fail(h, PM_ERR_VALIDATION, "L2 budget must lie in [1, 1024] MB");
+      h->batch_l2_mb = (int)value;
+      return PM_OK;
+    case PM_OPT_BATCH_CLUSTER_SIZE:
+      if (value < 0 || value > 8) return fail(h, PM_ERR_VALIDATION, "cluster size must lie in [0, 8]");
+      h->batch_force_cluster = (int)value;
+      return PM_OK;
+    case PM_OPT_BATCH_WARPS:
+      if (value != 0 && (value < 4 || value > 16))
+        return fail(h, PM_ERR_VALIDATION, "batch warps must be 0 or lie in [4, 16]");
+      h->batch_force_warps = (int)value;
+      return PM_OK;
+    case PM_OPT_BATCH_STAGES:
+      if (value < 0 || value > 2) return fail(h, PM_ERR_VALIDATION, "batch stages must lie in [0, 2]");
+      h->batch_force_stages = (int)value;
+      return PM_OK;
     case PM_OPT_KERNEL_TIMES:
       h->ktimes = value ? 1 : 0;
       h->krec.clear();
@@ -556,10 +584,42 @@ int pm_solve_batch_device_f64(pm_handle_t h, const double* a, const double* b, c
   if (r) return r;
   PM_CUDA(h, cudaSetDevice(h->device));
   h->launches = 0;
-  if ((r = build_plan(h, n, m, a, b, c, d, x, false, 0))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
+  pm::BatchPlan pl{};
+  if (batch > 1 && h->batch_cluster && aligned16(a) && aligned16(b) && aligned16(c) &&
+      aligned16(d) && aligned16(x) &&
+      pm::plan_batch(m, n_per_system, batch, h->sm_count, (int64_t)h->batch_l2_mb << 20,
+                     h->batch_force_cluster, h->batch_force_warps, h->batch_force_stages, &pl)) {
+    pm::BatchArgs A;
+    A.a = a; A.b = b; A.c = c; A.d = d; A.x = x;
+    A.n_sys = n_per_system;
+    A.batch = batch;
+    A.flag = h->dflag;
+    h->levels.clear();
+    h->last_batch_plan = pl;
+    const bool timed = h->ktimes && next_kevent(h) != nullptr;
+    const size_t ev = h->krec.size() * 2;
+    if (timed) cudaEventRecord(h->kev[ev], st);
+    PM_CUDA(h, pm::launch_batch_cluster(m, A, pl, st));
+    if (timed) {
+      cudaEventRecord(h->kev[ev + 1], st);
+      h->krec.push_back({4, 0, ev});
+    }
+    ++h->launches;
+    return PM_OK;
+  }
+  h->last_batch_plan = pm::BatchPlan{0, 0, 0, 0, 0, 0};
+  if ((r = build_plan(h, n, m, a, b, c, d, x, false, 0))) return r;
   return enq_full(h, st, batch > 1 ? n_per_system : 0);
+}
+
+int pm_last_batch_plan(pm_handle_t h, int32_t* out6) {
+  if (!h || !out6) return PM_ERR_VALIDATION;
+  const pm::BatchPlan& p = h->last_batch_plan;
+  out6[0] = p.cluster; out6[1] = p.warps; out6[2] = p.stages;
+  out6[3] = p.kmax; out6[4] = p.ntiles; out6[5] = p.clusters;
+  return PM_OK;
 }
 
 int pm_check(pm_handle_t h) {

@@ -21,10 +21,32 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-namespace pm {
+// One source, two precisions: the translation units compiled with
+// PM_REAL_F32 (pm_kernels_f32.cu) put the FP32 solver in namespace pm32,
+// the others the FP64 solver in namespace pm.
+#ifdef PM_REAL_F32
+#define PM_NS pm32
+#else
+#define PM_NS pm
+#endif
+
+namespace PM_NS {
+
+#ifdef PM_REAL_F32
+using real = float;
+using real2 = float2;
+__host__ __device__ __forceinline__ real2 make_real2(real x, real y) { return make_float2(x, y); }
+constexpr real kTinyPivot = 1e-35f;  // continuant magnitude below which the block
+                                     // falls back to the classic sweep
+#else
+using real = double;
+using real2 = double2;
+__host__ __device__ __forceinline__ real2 make_real2(real x, real y) { return make_double2(x, y); }
+constexpr real kTinyPivot = 1e-280;
+#endif
 
 struct Row {
-  double a, b, c, d;
+  real a, b, c, d;
 };
 struct Seg {
   Row F, L;
@@ -33,13 +55,13 @@ struct Seg {
 //   x[l1] = (p0 + p1*x[f1] + p2*x[l2]) * r
 //   x[f2] = (q0 + q1*x[f1] + q2*x[l2]) * r
 struct Node {
-  double p0, p1, p2, q0, q1, q2, r;
+  real p0, p1, p2, q0, q1, q2, r;
 };
 
-// Reciprocal: the MUFU seed (rcp.approx.ftz.f64) refined by two Newton steps
-// (<= 1 ulp), instead of the IEEE-rounded __drcp_rn sequence with its
-// slow-path branch.  A zero argument yields inf/NaN (and is flagged
-// separately by the callers).
+// Reciprocal: the MUFU seed (rcp.approx.ftz) refined by Newton steps -- two
+// for FP64, one for FP32 (<= 1 ulp) -- instead of the IEEE-rounded
+// __drcp_rn / __frcp_rn sequences with their slow-path branch.  A zero
+// argument yields inf/NaN (and is flagged separately by the callers).
 __device__ __forceinline__ double drcp(double x) {
 #ifdef PM_EXACT_RCP
   return __drcp_rn(x);
@@ -52,6 +74,16 @@ __device__ __forceinline__ double drcp(double x) {
   return fma(r, e, r);
 #endif
 }
+__device__ __forceinline__ float drcp(float x) {
+#ifdef PM_EXACT_RCP
+  return __frcp_rn(x);
+#else
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  const float e = fmaf(-x, r, 1.0f);
+  return fmaf(r, e, r);
+#endif
+}
 
 // 2^-(e(u) + e(v)), e = unbiased binary exponent: an exact power-of-two
 // scale that keeps u*v-sized products near 1 (clamped to the normal range).
@@ -62,6 +94,13 @@ __device__ __forceinline__ double pow2_inv_scale(double u, double v) {
   e = max(-1000, min(1000, e));
   return __hiloint2double((1023 - e) << 20, 0);
 }
+__device__ __forceinline__ float pow2_inv_scale(float u, float v) {
+  const int eu = (__float_as_int(u) >> 23) & 0xff;
+  const int ev = (__float_as_int(v) >> 23) & 0xff;
+  int e = eu + ev - 2 * 127;
+  e = max(-120, min(120, e));
+  return __int_as_float((127 - e) << 23);
+}
 
 // Merge segment A = [f1..l1] with its right neighbour B = [f2..l2], f2 = l1+1,
 // eliminating x[l1] and x[f2].  Division-free: both output equations are
@@ -71,10 +110,10 @@ __device__ __forceinline__ double pow2_inv_scale(double u, double v) {
 // reciprocal the downsweep needs is computed off that chain.
 __device__ __forceinline__ void combine(const Seg& A, const Seg& B, Seg& out, Node& nd,
                                         bool& bad) {
-  const double s = pow2_inv_scale(A.L.b, B.F.b);
-  const double det = fma(A.L.b, B.F.b, -A.L.c * B.F.a);
+  const real s = pow2_inv_scale(A.L.b, B.F.b);
+  const real det = fma(A.L.b, B.F.b, -A.L.c * B.F.a);
   bad |= (det == 0.0);
-  const double ds = det * s;
+  const real ds = det * s;
   nd.p0 = fma(B.F.b, A.L.d, -A.L.c * B.F.d) * s;
   nd.p1 = -(B.F.b * A.L.a) * s;
   nd.p2 = (A.L.c * B.F.c) * s;
@@ -95,8 +134,8 @@ __device__ __forceinline__ void combine(const Seg& A, const Seg& B, Seg& out, No
 }
 
 // Downsweep step of one node: (xf, xl) of the merged segment -> x[l1], x[f2].
-__device__ __forceinline__ void split_node(const Node& nd, double xf, double xl, double& xl1,
-                                           double& xf2) {
+__device__ __forceinline__ void split_node(const Node& nd, real xf, real xl, real& xl1,
+                                           real& xf2) {
   xl1 = fma(nd.p2, xl, fma(nd.p1, xf, nd.p0)) * nd.r;
   xf2 = fma(nd.q2, xl, fma(nd.q1, xf, nd.q0)) * nd.r;
 }
@@ -135,15 +174,15 @@ __device__ __forceinline__ Seg block_reduce(const Acc& r, int m_rt, bool& bad) {
     return S;
   }
   const int L = m - 2;
-  double den = r.b(1);
+  real den = r.b(1);
   bad |= (den == 0.0);
-  double inv = drcp(den);
-  double cp = (L > 1) ? r.c(1) * inv : 0.0;
-  double yp = r.d(1) * inv;
-  double gp = r.a(1) * inv;
-  double P = 1.0, Y1 = yp, G1 = gp;
+  real inv = drcp(den);
+  real cp = (L > 1) ? r.c(1) * inv : 0.0;
+  real yp = r.d(1) * inv;
+  real gp = r.a(1) * inv;
+  real P = 1.0, Y1 = yp, G1 = gp;
   auto step = [&](int j) {
-    const double aj = r.a(j);
+    const real aj = r.a(j);
     den = fma(-aj, cp, r.b(j));
     bad |= (den == 0.0);
     inv = drcp(den);
@@ -160,10 +199,10 @@ __device__ __forceinline__ Seg block_reduce(const Acc& r, int m_rt, bool& bad) {
   } else {
     for (int j = 2; j <= L; ++j) step(j);
   }
-  const double hL = r.c(L) * inv;
-  const double H1 = P * hL;
-  const double as = r.a(0), bs = r.b(0), cs = r.c(0), ds = r.d(0);
-  const double ae = r.a(m - 1), be = r.b(m - 1), ce = r.c(m - 1), de = r.d(m - 1);
+  const real hL = r.c(L) * inv;
+  const real H1 = P * hL;
+  const real as = r.a(0), bs = r.b(0), cs = r.c(0), ds = r.d(0);
+  const real ae = r.a(m - 1), be = r.b(m - 1), ce = r.c(m - 1), de = r.d(m - 1);
   S.F = Row{as, fma(-cs, G1, bs), -cs * H1, fma(-cs, Y1, ds)};
   S.L = Row{-ae * gp, fma(-ae, hL, be), ce, fma(-ae, yp, de)};
   return S;
@@ -189,7 +228,7 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
     return S;
   } else {
     constexpr int L = M - 2;
-    double q[L + 1], inv[L + 1];
+    real q[L + 1], inv[L + 1];
     q[0] = 1.0;
     q[1] = r.b(1);
     bool ok = q[1] != 0.0;
@@ -198,31 +237,31 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
       q[j] = fma(r.b(j), q[j - 1], -(r.a(j) * r.c(j - 1)) * q[j - 2]);
       ok &= (q[j] != 0.0);
     }
-    ok &= isfinite(q[L]) && (fabs(q[L]) > 1e-280);
+    ok &= isfinite(q[L]) && (fabs(q[L]) > kTinyPivot);
     if (ok) {
 #pragma unroll
       for (int j = 1; j <= L; ++j) inv[j] = q[j - 1] * drcp(q[j]);
     } else {  // classic sweep (rare)
-      double cprev = 0.0;
+      real cprev = 0.0;
 #pragma unroll
       for (int j = 1; j <= L; ++j) {
-        const double den = (j == 1) ? r.b(1) : fma(-r.a(j), cprev, r.b(j));
+        const real den = (j == 1) ? r.b(1) : fma(-r.a(j), cprev, r.b(j));
         bad |= (den == 0.0);
         inv[j] = drcp(den);
         cprev = r.c(j) * inv[j];
       }
     }
-    double cp = (L > 1) ? r.c(1) * inv[1] : 0.0;
-    double yp = r.d(1) * inv[1];
-    double gp = r.a(1) * inv[1];
-    double P = 1.0, Y1 = yp, G1 = gp;
+    real cp = (L > 1) ? r.c(1) * inv[1] : 0.0;
+    real yp = r.d(1) * inv[1];
+    real gp = r.a(1) * inv[1];
+    real P = 1.0, Y1 = yp, G1 = gp;
     if constexpr (KEEP) {
       r.set_b(1, inv[1]);
       if (L > 1) r.set_c(1, cp);
     }
 #pragma unroll
     for (int j = 2; j <= L; ++j) {
-      const double aj = r.a(j);
+      const real aj = r.a(j);
       P = -P * cp;
       yp = fma(-aj, yp, r.d(j)) * inv[j];
       gp = -aj * gp * inv[j];
@@ -234,10 +273,10 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
         if (j < L) r.set_c(j, cp);
       }
     }
-    const double hL = r.c(L) * inv[L];
-    const double H1 = P * hL;
-    const double as = r.a(0), bs = r.b(0), cs = r.c(0), ds = r.d(0);
-    const double ae = r.a(M - 1), be = r.b(M - 1), ce = r.c(M - 1), de = r.d(M - 1);
+    const real hL = r.c(L) * inv[L];
+    const real H1 = P * hL;
+    const real as = r.a(0), bs = r.b(0), cs = r.c(0), ds = r.d(0);
+    const real ae = r.a(M - 1), be = r.b(M - 1), ce = r.c(M - 1), de = r.d(M - 1);
     S.F = Row{as, fma(-cs, G1, bs), -cs * H1, fma(-cs, Y1, ds)};
     S.L = Row{-ae * gp, fma(-ae, hL, be), ce, fma(-ae, yp, de)};
     return S;
@@ -248,18 +287,18 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
 // reciprocals (an FMA + MUL chain per row), then back-substitution; x is
 // written over b(j).
 template <int M, class Acc>
-__device__ __forceinline__ void block_interior_kept(Acc& r, double xs, double xe) {
+__device__ __forceinline__ void block_interior_kept(Acc& r, real xs, real xe) {
   if constexpr (M == 2) {
     r.set_b(0, xs);
     r.set_b(1, xe);
   } else {
     constexpr int L = M - 2;
-    double dp[L + 1];
+    real dp[L + 1];
     dp[1] = fma(-r.a(1), xs, r.d(1)) * r.b(1);
 #pragma unroll
     for (int j = 2; j <= L; ++j) dp[j] = fma(-r.a(j), dp[j - 1], r.d(j)) * r.b(j);
     dp[L] = fma(-(r.c(L) * r.b(L)), xe, dp[L]);  // - h_L * x_e
-    double xn = dp[L];
+    real xn = dp[L];
     r.set_b(L, xn);
 #pragma unroll
     for (int j = L - 1; j >= 1; --j) {
@@ -275,7 +314,7 @@ __device__ __forceinline__ void block_interior_kept(Acc& r, double xs, double xe
 // x[e] = xe folded into the right-hand side.  Writes x(j) for j = 0..m-1
 // through r.set_x.  Acc must also provide scratch set_cp/cp, set_dp/dp.
 template <int M, class Acc>
-__device__ __forceinline__ void block_interior(Acc& r, int m_rt, double xs, double xe,
+__device__ __forceinline__ void block_interior(Acc& r, int m_rt, real xs, real xe,
                                                bool& bad) {
   const int m = (M > 0) ? M : m_rt;
   if (m == 2) {
@@ -284,17 +323,17 @@ __device__ __forceinline__ void block_interior(Acc& r, int m_rt, double xs, doub
     return;
   }
   const int L = m - 2;
-  double den = r.b(1);
+  real den = r.b(1);
   bad |= (den == 0.0);
-  double inv = drcp(den);
-  double rhs = fma(-r.a(1), xs, r.d(1));
+  real inv = drcp(den);
+  real rhs = fma(-r.a(1), xs, r.d(1));
   if (L == 1) rhs = fma(-r.c(1), xe, rhs);
-  double cp = (L > 1) ? r.c(1) * inv : 0.0;
-  double dp = rhs * inv;
+  real cp = (L > 1) ? r.c(1) * inv : 0.0;
+  real dp = rhs * inv;
   r.set_cp(1, cp);
   r.set_dp(1, dp);
   auto fwd = [&](int j) {
-    const double aj = r.a(j);
+    const real aj = r.a(j);
     den = fma(-aj, cp, r.b(j));
     bad |= (den == 0.0);
     inv = drcp(den);
@@ -305,7 +344,7 @@ __device__ __forceinline__ void block_interior(Acc& r, int m_rt, double xs, doub
     r.set_cp(j, cp);
     r.set_dp(j, dp);
   };
-  double xn;
+  real xn;
   auto bwd = [&](int j) {
     xn = fma(-r.cp(j), xn, r.dp(j));
     r.set_x(j, xn);
@@ -327,4 +366,4 @@ __device__ __forceinline__ void block_interior(Acc& r, int m_rt, double xs, doub
   r.set_x(m - 1, xe);
 }
 
-}  // namespace pm
+}  // namespace PM_NS

@@ -28,83 +28,9 @@
 
 #include "pm_device.cuh"
 #include "pm_kernels.h"
+#include "pm_tile.cuh"
 
-namespace pm {
-
-constexpr int kMaxStages = 4;
-// Stage 3 (level 0) keeps the block rows in its shared-memory stage: ~106
-// registers and a single stage per warp give 16 warps per SM, which hides
-// the sweeps' FP64 latency better than the register-resident variant.
-#ifndef PM_SOLVE_STAGE_ROWS
-#define PM_SOLVE_STAGE_ROWS 1
-#endif
-// ... and reads them as 16-byte pairs, recomputing the pivots in the
-// back-substitution instead of storing them (half the shared-memory traffic)
-#ifndef PM_SOLVE_PAIRS
-#define PM_SOLVE_PAIRS 1
-#endif
-#ifndef PM_REDUCE_PAIRS
-#define PM_REDUCE_PAIRS 0
-#endif
-constexpr int kMaxWarps = 8;  // P <= 256
-
-// ---------------------------------------------------------------------------
-// PTX helpers (mbarrier + bulk copies)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-// Programmatic dependent launch: let the next kernel of the stream start its
-// launch now, and wait for the previous one's results before touching them.
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+namespace PM_NS {
 
 bool g_use_pdl = true;
 
@@ -127,286 +53,16 @@ static cudaError_t launch_kernel(K kern, unsigned grid, unsigned block, size_t s
 
 void set_pdl(bool on) { g_use_pdl = on; }
 
-// ---------------------------------------------------------------------------
-// Row accessors
-// ---------------------------------------------------------------------------
-// Boundary fix-ups shared by both accessors (rows of one tile):
-//   local row >= valid      -> identity padding row (a=c=d=0, b=1)
-//   global row 0            -> a = 0   (a[0] is ignored by contract)
-//   global row n-1          -> c = 0   (c[n-1] is ignored by contract)
-//   odd tail row not covered by the 16-byte bulk copy -> read from global.
-struct TileCtx {
-  const double* ga;
-  const double* gb;
-  const double* gc;
-  const double* gd;
-  int64_t row0;   // first global row of the tile
-  int64_t n;      // rows of this level
-  int valid;      // rows of the tile inside [0, n)
-  bool odd_tail;  // row valid-1 must be read from global
-  bool zf, zl;    // zero a[0] / c[n-1]
-  int64_t sys_len;
-};
-
-// Does the block starting at tile row lr0 (m rows) need any fix-up?
-__device__ __forceinline__ bool block_needs_fixup(const TileCtx& t, int lr0, int m) {
-  const int64_t g0 = t.row0 + lr0;
-  if (g0 == 0 || g0 + m > t.n - 1) return true;
-  if (t.sys_len) {
-    const int64_t rem = g0 % t.sys_len;
-    return rem == 0 || rem + m > t.sys_len - 1;
-  }
-  return false;
-}
-
-__device__ __forceinline__ void fixup_row(const TileCtx& t, int lr, double& a, double& b,
-                                          double& c, double& d) {
-  if (lr >= t.valid) {
-    a = 0.0;
-    b = 1.0;
-    c = 0.0;
-    d = 0.0;
-    return;
-  }
-  const int64_t g = t.row0 + lr;
-  if (t.odd_tail && lr == t.valid - 1) {
-    a = __ldg(t.ga + g);
-    b = __ldg(t.gb + g);
-    c = __ldg(t.gc + g);
-    d = __ldg(t.gd + g);
-  }
-  if (t.zf && g == 0) a = 0.0;
-  if (t.zl && g == t.n - 1) c = 0.0;
-  if (t.sys_len) {
-    const int64_t rem = g % t.sys_len;
-    if (rem == 0) a = 0.0;
-    if (rem == t.sys_len - 1) c = 0.0;
-  }
-}
-
-// Compile-time m: the block's rows live in registers.
-template <int M>
-struct RegAcc {
-  double A[M], B[M], C[M], D[M];  // C/D are reused for c'/d' in Stage 3, B for x
-  __device__ __forceinline__ double a(int j) const { return A[j]; }
-  __device__ __forceinline__ double b(int j) const { return B[j]; }
-  __device__ __forceinline__ double c(int j) const { return C[j]; }
-  __device__ __forceinline__ double d(int j) const { return D[j]; }
-  __device__ __forceinline__ void set_cp(int j, double v) { C[j] = v; }
-  __device__ __forceinline__ double cp(int j) const { return C[j]; }
-  __device__ __forceinline__ void set_dp(int j, double v) { D[j] = v; }
-  __device__ __forceinline__ double dp(int j) const { return D[j]; }
-  __device__ __forceinline__ void set_x(int j, double v) { B[j] = v; }
-  __device__ __forceinline__ double x(int j) const { return B[j]; }
-  __device__ __forceinline__ void set_b(int j, double v) { B[j] = v; }
-  __device__ __forceinline__ void set_c(int j, double v) { C[j] = v; }
-
-  __device__ __forceinline__ void load(const double* sa, const double* sb, const double* sc,
-                                       const double* sd, int r0, const TileCtx& t) {
-    if constexpr ((M % 2) == 0) {
-      const double2* pa = reinterpret_cast<const double2*>(sa + r0);
-      const double2* pb = reinterpret_cast<const double2*>(sb + r0);
-      const double2* pc = reinterpret_cast<const double2*>(sc + r0);
-      const double2* pd = reinterpret_cast<const double2*>(sd + r0);
-#pragma unroll
-      for (int j = 0; j < M / 2; ++j) {
-        double2 va = pa[j], vb = pb[j], vc = pc[j], vd = pd[j];
-        A[2 * j] = va.x; A[2 * j + 1] = va.y;
-        B[2 * j] = vb.x; B[2 * j + 1] = vb.y;
-        C[2 * j] = vc.x; C[2 * j + 1] = vc.y;
-        D[2 * j] = vd.x; D[2 * j + 1] = vd.y;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        A[j] = sa[r0 + j]; B[j] = sb[r0 + j]; C[j] = sc[r0 + j]; D[j] = sd[r0 + j];
-      }
-    }
-    // rare: only blocks touching row 0, row n-1, a system boundary or the tail
-    if (block_needs_fixup(t, r0, M)) {
-#pragma unroll
-      for (int j = 0; j < M; ++j) fixup_row(t, r0 + j, A[j], B[j], C[j], D[j]);
-    }
-  }
-  // all four rows arrays back to the stage / raw reload (16-byte accesses:
-  // conflict-free at stride m = 10, unlike 8-byte ones)
-  __device__ __forceinline__ void store_rows(double* sa, double* sb, double* sc, double* sd,
-                                             int r0) const {
-    if constexpr ((M % 2) == 0) {
-#pragma unroll
-      for (int j = 0; j < M / 2; ++j) {
-        reinterpret_cast<double2*>(sa + r0)[j] = make_double2(A[2 * j], A[2 * j + 1]);
-        reinterpret_cast<double2*>(sb + r0)[j] = make_double2(B[2 * j], B[2 * j + 1]);
-        reinterpret_cast<double2*>(sc + r0)[j] = make_double2(C[2 * j], C[2 * j + 1]);
-        reinterpret_cast<double2*>(sd + r0)[j] = make_double2(D[2 * j], D[2 * j + 1]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        sa[r0 + j] = A[j]; sb[r0 + j] = B[j]; sc[r0 + j] = C[j]; sd[r0 + j] = D[j];
-      }
-    }
-  }
-  __device__ __forceinline__ void load_raw(const double* sa, const double* sb, const double* sc,
-                                           const double* sd, int r0) {
-    if constexpr ((M % 2) == 0) {
-#pragma unroll
-      for (int j = 0; j < M / 2; ++j) {
-        const double2 va = reinterpret_cast<const double2*>(sa + r0)[j];
-        const double2 vb = reinterpret_cast<const double2*>(sb + r0)[j];
-        const double2 vc = reinterpret_cast<const double2*>(sc + r0)[j];
-        const double2 vd = reinterpret_cast<const double2*>(sd + r0)[j];
-        A[2 * j] = va.x; A[2 * j + 1] = va.y; B[2 * j] = vb.x; B[2 * j + 1] = vb.y;
-        C[2 * j] = vc.x; C[2 * j + 1] = vc.y; D[2 * j] = vd.x; D[2 * j + 1] = vd.y;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < M; ++j) {
-        A[j] = sa[r0 + j]; B[j] = sb[r0 + j]; C[j] = sc[r0 + j]; D[j] = sd[r0 + j];
-      }
-    }
-  }
-  __device__ __forceinline__ void store_x(double* xbuf, int r0) const {
-    if constexpr ((M % 2) == 0) {
-      double2* px = reinterpret_cast<double2*>(xbuf + r0);
-#pragma unroll
-      for (int j = 0; j < M / 2; ++j) px[j] = make_double2(B[2 * j], B[2 * j + 1]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < M; ++j) xbuf[r0 + j] = B[j];
-    }
-  }
-};
-
-// Runtime m: rows stay in the shared-memory stage; c'/d' overwrite c/d in
-// place and x goes to the tile's x buffer.
-struct SmemAcc {
-  double* sa;
-  double* sb;
-  double* sc;
-  double* sd;
-  double* sx;
-  __device__ __forceinline__ double a(int j) const { return sa[j]; }
-  __device__ __forceinline__ double b(int j) const { return sb[j]; }
-  __device__ __forceinline__ double c(int j) const { return sc[j]; }
-  __device__ __forceinline__ double d(int j) const { return sd[j]; }
-  __device__ __forceinline__ void set_cp(int j, double v) { sc[j] = v; }
-  __device__ __forceinline__ double cp(int j) const { return sc[j]; }
-  __device__ __forceinline__ void set_dp(int j, double v) { sd[j] = v; }
-  __device__ __forceinline__ double dp(int j) const { return sd[j]; }
-  __device__ __forceinline__ void set_x(int j, double v) { sx[j] = v; }
-  __device__ __forceinline__ double x(int j) const { return sx[j]; }
-
-  __device__ __forceinline__ void fixup(int r0, int m, const TileCtx& t) {
-    if (block_needs_fixup(t, r0, m)) {
-      for (int j = 0; j < m; ++j) {
-        double a0 = sa[j], b0 = sb[j], c0 = sc[j], d0 = sd[j];
-        fixup_row(t, r0 + j, a0, b0, c0, d0);
-        sa[j] = a0; sb[j] = b0; sc[j] = c0; sd[j] = d0;
-      }
-    }
-  }
-};
-
-// Compile-time m, rows left in the shared-memory stage (fewer registers):
-// b/c slots are overwritten with 1/den and c' by block_reduce_fast<M, true>
-// and b with x by block_interior_kept.
-template <int M>
-struct StageAcc {
-  double* sa;
-  double* sb;
-  double* sc;
-  double* sd;
-  __device__ __forceinline__ double a(int j) const { return sa[j]; }
-  __device__ __forceinline__ double b(int j) const { return sb[j]; }
-  __device__ __forceinline__ double c(int j) const { return sc[j]; }
-  __device__ __forceinline__ double d(int j) const { return sd[j]; }
-  __device__ __forceinline__ void set_b(int j, double v) { sb[j] = v; }
-  __device__ __forceinline__ void set_c(int j, double v) { sc[j] = v; }
-  __device__ __forceinline__ double x(int j) const { return sb[j]; }
-};
-
-// Compile-time m, rows in the shared-memory stage, read as 16-byte pairs
-// (even m, pair-aligned rows): at stride m = 10 doubles a 16-byte access is
-// bank-conflict free where an 8-byte one is 2-way conflicted.  Within a
-// store-free stretch the compiler merges the two loads of a pair.
-template <int M>
-struct PairAcc {
-  const double* sa;
-  const double* sb;
-  const double* sc;
-  const double* sd;
-  __device__ __forceinline__ static double pick(const double* p, int j) {
-    if constexpr ((M % 2) == 0) {
-      const double2 v = *reinterpret_cast<const double2*>(p + (j & ~1));
-      return (j & 1) ? v.y : v.x;
-    } else {
-      return p[j];
-    }
-  }
-  __device__ __forceinline__ double a(int j) const { return pick(sa, j); }
-  __device__ __forceinline__ double b(int j) const { return pick(sb, j); }
-  __device__ __forceinline__ double c(int j) const { return pick(sc, j); }
-  __device__ __forceinline__ double d(int j) const { return pick(sd, j); }
-};
-
-// Stage 3 of one block straight from the stage: continuant pivots (as in
-// block_reduce_fast), forward substitution with x[s] = xs, x[e] = xe folded
-// in, back-substitution; x[0..M) returned in registers (all shared-memory
-// reads precede the caller's x stores).
-template <int M>
-__device__ __forceinline__ void block_solve_pairs(const PairAcc<M>& r, double xs, double xe,
-                                                  double (&x)[M], bool& bad) {
-  if constexpr (M == 2) {
-    x[0] = xs;
-    x[1] = xe;
-  } else {
-    constexpr int L = M - 2;
-    double q[L + 1], inv[L + 1], dp[L + 1];
-    q[0] = 1.0;
-    q[1] = r.b(1);
-    bool ok = q[1] != 0.0;
-#pragma unroll
-    for (int j = 2; j <= L; ++j) {
-      q[j] = fma(r.b(j), q[j - 1], -(r.a(j) * r.c(j - 1)) * q[j - 2]);
-      ok &= (q[j] != 0.0);
-    }
-    ok &= isfinite(q[L]) && (fabs(q[L]) > 1e-280);
-    if (ok) {
-#pragma unroll
-      for (int j = 1; j <= L; ++j) inv[j] = q[j - 1] * drcp(q[j]);
-    } else {
-      double cprev = 0.0;
-#pragma unroll
-      for (int j = 1; j <= L; ++j) {
-        const double den = (j == 1) ? r.b(1) : fma(-r.a(j), cprev, r.b(j));
-        bad |= (den == 0.0);
-        inv[j] = drcp(den);
-        cprev = r.c(j) * inv[j];
-      }
-    }
-    dp[1] = fma(-r.a(1), xs, r.d(1)) * inv[1];
-#pragma unroll
-    for (int j = 2; j <= L; ++j) dp[j] = fma(-r.a(j), dp[j - 1], r.d(j)) * inv[j];
-    dp[L] = fma(-(r.c(L) * inv[L]), xe, dp[L]);
-    x[L] = dp[L];
-#pragma unroll
-    for (int j = L - 1; j >= 1; --j) x[j] = fma(-(r.c(j) * inv[j]), x[j + 1], dp[j]);
-    x[0] = xs;
-    x[M - 1] = xe;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // CTA combine tree
 // ---------------------------------------------------------------------------
 struct TreeSmem {
   Seg wseg[kMaxWarps];
-  double2 wx[kMaxWarps];
+  real2 wx[kMaxWarps];
   Node cnodes[kMaxWarps];
 };
 
-__device__ __forceinline__ int warp_node_off(int k) { return 32 - (32 >> k); }
 
 // Upsweep.  Leaves: one segment per thread.  Result valid in thread 0.
 // Stores Node coefficients when `wnodes` is non-null.
@@ -445,31 +101,9 @@ __device__ __forceinline__ Seg cta_upsweep(Seg s, TreeSmem& tr, Node* wnodes, in
   return s;
 }
 
-// One downsweep level inside a warp: lanes that were left operands at
-// stride `stride` split their (xf, xl) with the stored node and hand the
-// right half to lane + stride.
-__device__ __forceinline__ void down_level(const Node* nodes, int stride, int lane, int active,
-                                           bool right_nonempty, double& xf, double& xl) {
-  const bool left = lane < active && (lane & (2 * stride - 1)) == 0 && right_nonempty;
-  double sf = 0.0, sl = 0.0;
-  if (left) {
-    double xl1, xf2;
-    split_node(nodes[lane / (2 * stride)], xf, xl, xl1, xf2);
-    sf = xf2;
-    sl = xl;
-    xl = xl1;
-  }
-  const double rf = __shfl_up_sync(0xffffffffu, sf, stride);
-  const double rl = __shfl_up_sync(0xffffffffu, sl, stride);
-  if (lane < active && (lane & (2 * stride - 1)) == stride) {
-    xf = rf;
-    xl = rl;
-  }
-}
-
 // Downsweep.  (xf, xl) of the tile are valid in thread 0 on entry; on exit
 // every thread holds (x_s, x_e) of its own block.
-__device__ __forceinline__ void cta_downsweep(double& xf, double& xl, TreeSmem& tr,
+__device__ __forceinline__ void cta_downsweep(real& xf, real& xl, TreeSmem& tr,
                                               const Node* wnodes, int lane, int warp, int nwarps,
                                               int nblk) {
   if (nwarps > 1) {
@@ -479,10 +113,10 @@ __device__ __forceinline__ void cta_downsweep(double& xf, double& xl, TreeSmem& 
       for (int k = levels - 1; k >= 0; --k)
         down_level(tr.cnodes + (nwarps - (nwarps >> k)), 1 << k, lane, nwarps,
                    (lane + (1 << k)) * 32 < nblk, xf, xl);
-      if (lane < nwarps) tr.wx[lane] = make_double2(xf, xl);
+      if (lane < nwarps) tr.wx[lane] = make_real2(xf, xl);
     }
     __syncthreads();
-    const double2 v = tr.wx[warp];
+    const real2 v = tr.wx[warp];
     xf = v.x;
     xl = v.y;
   }
@@ -509,8 +143,8 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
   const int S = BULK ? args.stages : 1;
   const int r0 = tid * m;
 
-  double* stage0 = reinterpret_cast<double*>(smem_raw);
-  double* xbuf = stage0 + (size_t)S * 4 * T;
+  real* stage0 = reinterpret_cast<real*>(smem_raw);
+  real* xbuf = stage0 + (size_t)S * 4 * T;
   Node* wnodes = reinterpret_cast<Node*>(xbuf + (MODE == kModeReduce ? 0 : T));
 
   const int64_t ntiles = args.tile_end - args.tile_begin;
@@ -520,12 +154,12 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     const int64_t idx = blockIdx.x + k * gridDim.x;
     return args.reverse ? (args.tile_end - 1 - idx) : (args.tile_begin + idx);
   };
-  auto stage_ptr = [&](int s, int q) -> double* { return stage0 + ((size_t)s * 4 + q) * T; };
+  auto stage_ptr = [&](int s, int q) -> real* { return stage0 + ((size_t)s * 4 + q) * T; };
 
   auto issue = [&](int s, int64_t t) {
     const int64_t row0 = t * T;
     const int64_t v = (args.n - row0 < T) ? (args.n - row0) : T;
-    const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(1)) * 8);
+    const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(kBulkRows - 1)) * sizeof(real));
     fence_proxy_async();
     mbar_arrive_expect_tx(&bars[s], 4u * bytes);
     if (bytes) {
@@ -557,16 +191,16 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     ctx.row0 = t * T;
     ctx.n = args.n;
     ctx.valid = static_cast<int>((args.n - ctx.row0 < T) ? (args.n - ctx.row0) : T);
-    ctx.odd_tail = BULK && (ctx.valid & 1);
+    ctx.bulk_rows = BULK ? (ctx.valid & ~(kBulkRows - 1)) : ctx.valid;
     ctx.zf = args.zero_first != 0;
     ctx.zl = args.zero_last != 0;
     ctx.sys_len = args.sys_len;
     // non-empty leaf blocks of this tile (pad mode: all P)
     const int nblk = args.pad_mode ? P : (ctx.valid + m - 1) / m;
-    double* sa = stage_ptr(s, 0);
-    double* sb = stage_ptr(s, 1);
-    double* sc = stage_ptr(s, 2);
-    double* sd = stage_ptr(s, 3);
+    real* sa = stage_ptr(s, 0);
+    real* sb = stage_ptr(s, 1);
+    real* sc = stage_ptr(s, 2);
+    real* sd = stage_ptr(s, 3);
 
     if constexpr (BULK) {
       mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
@@ -614,13 +248,13 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
         args.rc[2 * t + 1] = top.L.c; args.rd[2 * t + 1] = top.L.d;
       }
     } else {
-      double xf = 0.0, xl = 0.0;
+      real xf = 0.0, xl = 0.0;
       if (tid == 0) {
         if constexpr (MODE == kModeRoot) {
           // top.F.a and top.L.c multiply unknowns outside the system (zero).
-          const double det = fma(top.F.b, top.L.b, -top.F.c * top.L.a);
+          const real det = fma(top.F.b, top.L.b, -top.F.c * top.L.a);
           bad |= (det == 0.0);
-          const double inv = drcp(det);
+          const real inv = drcp(det);
           xf = fma(top.F.d, top.L.b, -top.F.c * top.L.d) * inv;
           xl = fma(top.F.b, top.L.d, -top.L.a * top.F.d) * inv;
         } else {
@@ -638,22 +272,22 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
 #pragma unroll
         for (int j = 0; j < M; ++j) bad |= !isfinite(regs.x(j));
         regs.store_x(xbuf, r0);
-        if (ctx.odd_tail && r0 <= ctx.valid - 1 && ctx.valid - 1 < r0 + M) {
+        if (r0 + M > ctx.bulk_rows && r0 < ctx.valid) {  // tail rows: not in the bulk store
 #pragma unroll
           for (int j = 0; j < M; ++j)
-            if (r0 + j == ctx.valid - 1) args.x[ctx.row0 + r0 + j] = regs.x(j);
+            if (r0 + j >= ctx.bulk_rows && r0 + j < ctx.valid) args.x[ctx.row0 + r0 + j] = regs.x(j);
         }
       } else {
         block_interior<0>(sacc, m, xf, xl, bad);
         for (int j = 0; j < m; ++j) bad |= !isfinite(sacc.x(j));
-        if (ctx.odd_tail && r0 <= ctx.valid - 1 && ctx.valid - 1 < r0 + m)
-          args.x[ctx.row0 + ctx.valid - 1] = sacc.x(ctx.valid - 1 - r0);
+        for (int j = (ctx.bulk_rows > r0 ? ctx.bulk_rows - r0 : 0); j < m && r0 + j < ctx.valid; ++j)
+          args.x[ctx.row0 + r0 + j] = sacc.x(j);  // tail rows: not in the bulk store
       }
       if constexpr (BULK) {
         fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
-          const uint32_t bytes = static_cast<uint32_t>((ctx.valid & ~1) * 8);
+          const uint32_t bytes = static_cast<uint32_t>(ctx.bulk_rows * sizeof(real));
           if (bytes) {
             bulk_s2g(args.x + ctx.row0, xbuf, bytes);
             bulk_commit();
@@ -683,26 +317,7 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
 // warp's next tiles are in flight while it computes.  The tile's reduced rows
 // go to the level above, which uses the CTA-tile kernel.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ Seg warp_upsweep(Seg s, Node* nodes, int lane, int nblk, bool& bad) {
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int stride = 1 << k;
-    Seg o = shfl_down_seg(s, stride);
-    if ((lane & (2 * stride - 1)) == 0 && lane + stride < nblk) {
-      Node nd;
-      combine(s, o, s, nd, bad);
-      if (nodes) nodes[warp_node_off(k) + (lane >> (k + 1))] = nd;
-    }
-  }
-  return s;
-}
 
-__device__ __forceinline__ void warp_downsweep(double& xf, double& xl, const Node* nodes, int lane,
-                                               int nblk) {
-#pragma unroll
-  for (int k = 4; k >= 0; --k)
-    down_level(nodes + warp_node_off(k), 1 << k, lane, 32, lane + (1 << k) < nblk, xf, xl);
-}
 
 // Per-warp shared memory: [stages][a,b,c,d][T] | x buffer | 31 tree nodes | mbarriers.
 // The x buffer exists only for Stage 3 with rows in registers (runtime m).
@@ -713,7 +328,7 @@ __host__ __device__ size_t warp_xbuf_doubles(int mode, int m) {
 
 __host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages) {
   const size_t T = (size_t)32 * m;
-  size_t bytes = (size_t)stages * 4 * T * sizeof(double) + warp_xbuf_doubles(mode, m) * sizeof(double) +
+  size_t bytes = (size_t)stages * 4 * T * sizeof(real) + warp_xbuf_doubles(mode, m) * sizeof(real) +
                  31 * sizeof(Node) + 2 * kMaxStages * sizeof(uint64_t);
   return (bytes + 127) / 128 * 128;
 }
@@ -755,8 +370,8 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
   const int r0 = lane * m;
   const size_t per_warp = warp_smem_bytes(MODE, m, S);
   unsigned char* base = smem_raw + per_warp * warp;
-  double* stage0 = reinterpret_cast<double*>(base);
-  double* xbuf = stage0 + (size_t)S * 4 * T;
+  real* stage0 = reinterpret_cast<real*>(base);
+  real* xbuf = stage0 + (size_t)S * 4 * T;
   Node* nodes = reinterpret_cast<Node*>(xbuf + warp_xbuf_doubles(MODE, m));
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + per_warp - 2 * kMaxStages * sizeof(uint64_t));
 
@@ -808,11 +423,11 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       return tile_of(kk);
     }
   };
-  auto stage_ptr = [&](int s, int q) -> double* { return stage0 + ((size_t)s * 4 + q) * T; };
+  auto stage_ptr = [&](int s, int q) -> real* { return stage0 + ((size_t)s * 4 + q) * T; };
   auto issue = [&](int s, int64_t t) {
     const int64_t row0 = t * T;
     const int64_t v = (args.n - row0 < T) ? (args.n - row0) : T;
-    const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(1)) * 8);
+    const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(kBulkRows - 1)) * sizeof(real));
     fence_proxy_async();
     mbar_arrive_expect_tx(&bars[s], 4u * bytes);
     if (bytes) {
@@ -841,8 +456,8 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
   // backwards from the chunk's two values -- the node stored by Stage 1 for
   // tile t splits (x_first(chunk), x_last(tiles lo..t)) into
   // x_last(tiles lo..t-1) and x_first(tile t).
-  double xf_next = 0.0, xl_next = 0.0;
-  double xf_chunk = 0.0, xl_run = 0.0;
+  real xf_next = 0.0, xl_next = 0.0;
+  real xf_chunk = 0.0, xl_run = 0.0;
   Node nd_next{};
   if (MODE != kModeReduce && nlocal > 0) {
     if constexpr (CHAIN) {
@@ -868,7 +483,7 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       t = tile_of(k);
     }
     const int s = static_cast<int>(k % S);
-    double xf_tile = xf_next, xl_tile = xl_next;
+    real xf_tile = xf_next, xl_tile = xl_next;
     if constexpr (MODE != kModeReduce) {
       if constexpr (CHAIN) {
         if (lane == 0) {
@@ -880,7 +495,7 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
             xf_tile = xf_chunk;
             xl_tile = xl_run;
           } else {
-            double xl_prev, xf_t;
+            real xl_prev, xf_t;
             split_node(nd_next, xf_chunk, xl_run, xl_prev, xf_t);
             xf_tile = xf_t;
             xl_tile = xl_run;
@@ -903,15 +518,15 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     ctx.row0 = t * T;
     ctx.n = args.n;
     ctx.valid = static_cast<int>((args.n - ctx.row0 < T) ? (args.n - ctx.row0) : T);
-    ctx.odd_tail = (ctx.valid & 1);
+    ctx.bulk_rows = ctx.valid & ~(kBulkRows - 1);
     ctx.zf = args.zero_first != 0;
     ctx.zl = args.zero_last != 0;
     ctx.sys_len = args.sys_len;
     const int nblk = args.pad_mode ? 32 : (ctx.valid + m - 1) / m;
-    double* sa = stage_ptr(s, 0);
-    double* sb = stage_ptr(s, 1);
-    double* sc = stage_ptr(s, 2);
-    double* sd = stage_ptr(s, 3);
+    real* sa = stage_ptr(s, 0);
+    real* sb = stage_ptr(s, 1);
+    real* sc = stage_ptr(s, 2);
+    real* sd = stage_ptr(s, 3);
     mbar_wait(&bars[s], static_cast<uint32_t>((k / S) & 1));
 
     Seg seg;
@@ -981,14 +596,14 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
         args.rc[2 * t + 1] = top.L.c; args.rd[2 * t + 1] = top.L.d;
       }
     } else {
-      double xf = xf_tile, xl = xl_tile;
+      real xf = xf_tile, xl = xl_tile;
       __syncwarp();  // nodes written by lanes are read by the same lanes only
       warp_downsweep(xf, xl, nodes, lane, nblk);
-      const double* xsrc = kStageRows ? sb : xbuf;
+      const real* xsrc = kStageRows ? sb : xbuf;
       if constexpr (kStageRows) {
 #if PM_SOLVE_PAIRS
         const PairAcc<(M > 0 ? M : 1)> pa{sa + r0, sb + r0, sc + r0, sd + r0};
-        double xv[(M > 0 ? M : 1)];
+        real xv[(M > 0 ? M : 1)];
         block_solve_pairs<(M > 0 ? M : 1)>(pa, xf, xl, xv, bad);
         __syncwarp();
 #pragma unroll
@@ -996,7 +611,7 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
         if constexpr ((M % 2) == 0) {
 #pragma unroll
           for (int j = 0; j < M / 2; ++j)
-            reinterpret_cast<double2*>(sb + r0)[j] = make_double2(xv[2 * j], xv[2 * j + 1]);
+            reinterpret_cast<real2*>(sb + r0)[j] = make_real2(xv[2 * j], xv[2 * j + 1]);
         } else {
 #pragma unroll
           for (int j = 0; j < M; ++j) sb[r0 + j] = xv[j];
@@ -1017,11 +632,11 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       }
       __syncwarp();
       // coalesced store of the tile's x
-      double* gx = args.x + ctx.row0;
+      real* gx = args.x + ctx.row0;
       const int v = ctx.valid;
-      if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & 15) == 0)) {
-        const double2* s2 = reinterpret_cast<const double2*>(xsrc);
-        double2* g2 = reinterpret_cast<double2*>(gx);
+      if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & (sizeof(real2) - 1)) == 0)) {
+        const real2* s2 = reinterpret_cast<const real2*>(xsrc);
+        real2* g2 = reinterpret_cast<real2*>(gx);
         for (int i = lane; i < v / 2; i += 32) g2[i] = s2[i];
       } else {
         for (int i = lane; i < v; i += 32) gx[i] = xsrc[i];
@@ -1126,15 +741,15 @@ int warp_kernel_ctas_per_sm(int mode, int m, int stages, int warps_per_cta, bool
 // final 2x2 (rank 0's F.a and rank world-1's L.c are zero), then walk the
 // chain back down to this rank.
 // ---------------------------------------------------------------------------
-__global__ void dist_chain_kernel(const double* __restrict__ iface, int world, int rank,
-                                  double* __restrict__ xb, int* flag) {
+__global__ void dist_chain_kernel(const real* __restrict__ iface, int world, int rank,
+                                  real* __restrict__ xb, int* flag) {
   extern __shared__ Node chain_nodes[];
   if (threadIdx.x != 0) return;
   bool bad = false;
   // per rank: [Fa, La, Fb, Lb, Fc, Lc, Fd, Ld] (the REDUCE kernel's output
   // layout for a one-tile level: ra = p, rb = p + 2, rc = p + 4, rd = p + 6)
   auto seg_of = [&](int k) {
-    const double* p = iface + 8 * k;
+    const real* p = iface + 8 * k;
     return Seg{Row{p[0], p[2], p[4], p[6]}, Row{p[1], p[3], p[5], p[7]}};
   };
   Seg acc = seg_of(0);
@@ -1143,14 +758,14 @@ __global__ void dist_chain_kernel(const double* __restrict__ iface, int world, i
     combine(acc, seg_of(k), acc, nd, bad);
     chain_nodes[k] = nd;
   }
-  const double det = fma(acc.F.b, acc.L.b, -acc.F.c * acc.L.a);
+  const real det = fma(acc.F.b, acc.L.b, -acc.F.c * acc.L.a);
   bad |= (det == 0.0);
-  const double inv = drcp(det);
-  const double x0 = fma(acc.F.d, acc.L.b, -acc.F.c * acc.L.d) * inv;  // x_first of rank 0
-  double xl = fma(acc.F.b, acc.L.d, -acc.L.a * acc.F.d) * inv;        // x_last of rank k
-  double xf = x0;
+  const real inv = drcp(det);
+  const real x0 = fma(acc.F.d, acc.L.b, -acc.F.c * acc.L.d) * inv;  // x_first of rank 0
+  real xl = fma(acc.F.b, acc.L.d, -acc.L.a * acc.F.d) * inv;        // x_last of rank k
+  real xf = x0;
   for (int k = world - 1; k >= 1 && k >= rank; --k) {
-    double xl_prev, xf_k;
+    real xl_prev, xf_k;
     split_node(chain_nodes[k], x0, xl, xl_prev, xf_k);
     if (k == rank) {
       xf = xf_k;
@@ -1163,7 +778,7 @@ __global__ void dist_chain_kernel(const double* __restrict__ iface, int world, i
   if (bad || !isfinite(xf) || !isfinite(xl)) atomicOr(flag, 1);
 }
 
-cudaError_t launch_dist_chain(const double* iface_all, int world, int rank, double* xb, int* flag,
+cudaError_t launch_dist_chain(const real* iface_all, int world, int rank, real* xb, int* flag,
                               cudaStream_t st) {
   const size_t smem = (size_t)world * sizeof(Node);
   if (smem > 48 * 1024) return cudaErrorInvalidValue;
@@ -1180,7 +795,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
-__global__ void generate_kernel(double* a, double* b, double* c, double* d, int64_t n,
+__global__ void generate_kernel(real* a, real* b, real* c, real* d, int64_t n,
                                 int64_t row0, int64_t count, uint64_t ka, uint64_t kb,
                                 uint64_t kc, uint64_t kd, uint64_t ks) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count;
@@ -1195,10 +810,12 @@ __global__ void generate_kernel(double* a, double* b, double* c, double* d, int6
     const double ci = (i == n - 1) ? 0.0 : __dadd_rn(__dmul_rn(2.0, uc), -1.0);
     const double mag = __dadd_rn(__dadd_rn(__dadd_rn(fabs(ai), fabs(ci)), 1.0), ub);
     const double bi = (splitmix64(ks + u) >> 63) ? -mag : mag;
-    if (a) a[k] = ai;
-    if (b) b[k] = bi;
-    if (c) c[k] = ci;
-    if (d) d[k] = __dadd_rn(__dmul_rn(2.0, ud), -1.0);
+    // FP64 values (bit-identical to the oracle); the FP32 solver's inputs are
+    // their round-to-nearest FP32 images
+    if (a) a[k] = static_cast<real>(ai);
+    if (b) b[k] = static_cast<real>(bi);
+    if (c) c[k] = static_cast<real>(ci);
+    if (d) d[k] = static_cast<real>(__dadd_rn(__dmul_rn(2.0, ud), -1.0));
   }
 }
 
@@ -1212,7 +829,7 @@ static uint64_t key_host(uint64_t seed, uint64_t arr) {
   return splitmix64_host(seed ^ (0x632BE59BD9B4E019ull * (arr + 1ull)));
 }
 
-cudaError_t launch_generate(double* a, double* b, double* c, double* d, int64_t n,
+cudaError_t launch_generate(real* a, real* b, real* c, real* d, int64_t n,
                             int64_t row0, int64_t count, uint64_t seed, int sm_count,
                             cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
@@ -1231,9 +848,9 @@ cudaError_t launch_generate(double* a, double* b, double* c, double* d, int64_t 
 // ---------------------------------------------------------------------------
 size_t tile_smem_bytes(int mode, int P, int m, int stages) {
   const size_t T = (size_t)P * m;
-  size_t bytes = (size_t)stages * 4 * T * sizeof(double);
+  size_t bytes = (size_t)stages * 4 * T * sizeof(real);
   if (mode != kModeReduce) {
-    bytes += T * sizeof(double);                          // x buffer
+    bytes += T * sizeof(real);                          // x buffer
     bytes += (size_t)(P / 32) * 31 * sizeof(Node);        // warp-level nodes
   }
   return bytes;
@@ -1292,4 +909,4 @@ cudaError_t launch_tile_kernel(int mode, const TileArgs& args, int P, bool bulk,
               : dispatch_m<kModeRoot, false>(Mspec, args, P, sm_count, st, grid_out);
 }
 
-}  // namespace pm
+}  // namespace PM_NS

@@ -60,6 +60,34 @@ class DistributedSolver:
         else:
             self.dist.all_gather_into_tensor(self.iface_all, self.iface, group=self.group)
 
+    def solve_host(self, a, b, c, d, x, m: int = 10, stream=None):
+        """End-to-end collective solve from this rank's host rows (page-locked
+        numpy arrays, e.g. `pinned_empty`): H2D of a, b, c, d into device
+        staging owned by this object, the row-sharded solve, D2H of x.
+        Synchronous; returns x."""
+        import numpy as np
+        import torch
+
+        n = int(len(b))
+        for t in (a, b, c, d, x):
+            if not (isinstance(t, np.ndarray) and t.dtype == np.float64 and t.flags.c_contiguous
+                    and len(t) == n):
+                raise ValidationError("host arrays must be contiguous float64 of equal length")
+        dev = self.iface.device
+        if getattr(self, "_stage", None) is None or self._stage.shape[1] < n:
+            self._stage = torch.empty((5, n), dtype=torch.float64, device=dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        da, db, dc, dd, dx = (self._stage[k, :n] for k in range(5))
+        with torch.cuda.stream(st):
+            for dst, src in ((da, a), (db, b), (dc, c), (dd, d)):
+                dst.copy_(torch.from_numpy(src), non_blocking=True)
+            self.solve(da, db, dc, dd, dx, m=m, stream=st)
+            xh = torch.from_numpy(x)
+            xh.copy_(dx, non_blocking=True)
+        st.synchronize()
+        self.solver.check()
+        return x
+
     def solve(self, a, b, c, d, x, m: int = 10, stream=None):
         self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
         self._all_gather()

@@ -30,6 +30,11 @@ PM_OPT_CHAIN = 10
 PM_OPT_UPPER_M = 11
 PM_OPT_ROOT_M = 12
 PM_OPT_PDL = 13
+PM_OPT_BATCH_CLUSTER = 14
+PM_OPT_BATCH_L2_MB = 15
+PM_OPT_BATCH_CLUSTER_SIZE = 16
+PM_OPT_BATCH_WARPS = 17
+PM_OPT_BATCH_STAGES = 18
 PM_MAX_M = 128
 
 
@@ -122,6 +127,12 @@ class PartitionSolver:
     @property
     def last_launch_count(self) -> int:
         return int(self._L.pm_last_launch_count(self._h))
+
+    def last_batch_plan(self) -> dict:
+        """Cluster-kernel configuration of the last batch solve (zeros: level kernels)."""
+        out = (C.c_int32 * 6)()
+        self._L.pm_last_batch_plan(self._h, out)
+        return dict(zip(("cluster", "warps", "stages", "kmax", "ntiles", "clusters"), list(out)))
 
     def last_plan(self) -> list[int]:
         buf = (C.c_int64 * 16)()

@@ -169,6 +169,99 @@ def test_batch(solver, nps, batch, m):
         _check(x[k * nps:(k + 1) * nps], *s)
 
 
+def _batch_systems(nps, batch, seed):
+    rng = np.random.default_rng(seed)
+    systems = [oracle.generate(nps, int(s)) for s in rng.integers(0, 2**31, batch)]
+    cat = [np.concatenate([s[k] for s in systems]) for k in range(4)]
+    for k in range(batch):  # ignored corners: poison them
+        cat[0][k * nps] = 9.0
+        cat[2][k * nps + nps - 1] = -9.0
+    return systems, cat
+
+
+@pytest.mark.parametrize("cluster_opt", [0, 1])
+@pytest.mark.parametrize("nps,batch,m", [
+    (100_000, 40, 10), (640, 7, 10), (642, 9, 10), (20_002, 13, 10), (99_998, 5, 8), (4_096, 11, 2),
+    (65_536, 6, 16), (655_360, 3, 10), (3_000_000, 2, 10), (5_001, 4, 10), (319, 3, 10)])
+def test_batch_cluster_kernel(solver, cluster_opt, nps, batch, m):
+    """Cluster-per-system kernel (PM_OPT_BATCH_CLUSTER) vs the oracle; odd or
+    one-tile systems and oversize CTA ranges fall back to the level kernels."""
+    import torch
+    from paper_2501_05938_b200.solver import PM_OPT_BATCH_CLUSTER
+
+    systems, cat = _batch_systems(nps, batch, nps * 7 + batch)
+    t = [torch.from_numpy(v).cuda() for v in cat]
+    solver.set_option(PM_OPT_BATCH_CLUSTER, cluster_opt)
+    try:
+        x = solver.solve_batch_device(*t, n_per_system=nps, m=m).cpu().numpy()
+        solver.check()
+        plan = solver.last_batch_plan()
+    finally:
+        solver.set_option(PM_OPT_BATCH_CLUSTER, 0)
+    nt = -(-nps // (32 * m))  # tiles per system
+    if cluster_opt and nps % 2 == 0 and 2 <= nt <= 600:
+        assert plan["cluster"] > 0, plan
+    if not cluster_opt or nps % 2 or nt < 2 or nt > 8 * 256:
+        assert plan["cluster"] == 0, plan
+    for k, s in enumerate(systems):
+        _check(x[k * nps:(k + 1) * nps], *s)
+
+
+@pytest.mark.parametrize("cl", [1, 2, 3, 5, 7, 8])
+@pytest.mark.parametrize("warps", [4, 9, 14])
+def test_batch_cluster_shapes(solver, cl, warps):
+    """Every cluster size / warp count gives the same (checked) answer."""
+    import torch
+    from paper_2501_05938_b200.solver import (PM_OPT_BATCH_CLUSTER, PM_OPT_BATCH_CLUSTER_SIZE,
+                                              PM_OPT_BATCH_WARPS)
+
+    nps, batch, m = 12_000, 10, 10
+    systems, cat = _batch_systems(nps, batch, 5)
+    t = [torch.from_numpy(v).cuda() for v in cat]
+    solver.set_option(PM_OPT_BATCH_CLUSTER, 1)
+    solver.set_option(PM_OPT_BATCH_CLUSTER_SIZE, cl)
+    solver.set_option(PM_OPT_BATCH_WARPS, warps)
+    try:
+        x = solver.solve_batch_device(*t, n_per_system=nps, m=m).cpu().numpy()
+        solver.check()
+        plan = solver.last_batch_plan()
+    finally:
+        solver.set_option(PM_OPT_BATCH_CLUSTER, 0)
+        solver.set_option(PM_OPT_BATCH_CLUSTER_SIZE, 0)
+        solver.set_option(PM_OPT_BATCH_WARPS, 0)
+    assert plan["cluster"] == cl and plan["warps"] == warps, plan
+    for k, s in enumerate(systems):
+        _check(x[k * nps:(k + 1) * nps], *s)
+
+
+def test_batch_cluster_aliasing_and_zero_pivot(solver):
+    import torch
+
+    from paper_2501_05938_b200 import errors
+
+    from paper_2501_05938_b200.solver import PM_OPT_BATCH_CLUSTER
+
+    nps, batch = 20_000, 6
+    systems, cat = _batch_systems(nps, batch, 11)
+    t = [torch.from_numpy(v).cuda() for v in cat]
+    solver.set_option(PM_OPT_BATCH_CLUSTER, 1)
+    try:
+        x = solver.solve_batch_device(*t, n_per_system=nps, m=10, out=t[3]).cpu().numpy()  # x = d
+        solver.check()
+        assert solver.last_batch_plan()["cluster"] > 0
+        for k, s in enumerate(systems):
+            _check(x[k * nps:(k + 1) * nps], *s)
+        cat[1][3 * nps + 5] = 0.0  # b = 0 inside a block interior of system 3
+        cat[0][3 * nps + 5] = 0.0
+        cat[2][3 * nps + 5] = 0.0
+        t = [torch.from_numpy(v).cuda() for v in cat]
+        solver.solve_batch_device(*t, n_per_system=nps, m=10)
+        with pytest.raises(errors.ComputationError):
+            solver.check()
+    finally:
+        solver.set_option(PM_OPT_BATCH_CLUSTER, 0)
+
+
 def test_batch_config4_sample(solver):
     """BASELINE config 4 on one GPU: 4096 x 1e5, sampled systems checked."""
     import torch
@@ -188,6 +281,31 @@ def test_batch_config4_sample(solver):
         sa[0] = 0.0
         sc[-1] = 0.0
         _check(xh[sl], sa, bh[sl].copy(), sc, dh[sl].copy())
+
+
+def test_batch_config4_cluster_kernel(solver):
+    """Config 4 through the cluster-per-system kernel, sampled systems checked."""
+    import torch
+    from paper_2501_05938_b200.solver import PM_OPT_BATCH_CLUSTER
+
+    nps, batch = 100_000, 4096
+    a, b, c, d = solver.generate_device(nps * batch, 99)
+    solver.set_option(PM_OPT_BATCH_CLUSTER, 1)
+    try:
+        x = solver.solve_batch_device(a, b, c, d, n_per_system=nps, m=10)
+        solver.check()
+        assert solver.last_batch_plan()["cluster"] > 0
+    finally:
+        solver.set_option(PM_OPT_BATCH_CLUSTER, 0)
+    xh = x.cpu().numpy()
+    for k in (0, 5, 2047, 4095):
+        sl = slice(k * nps, (k + 1) * nps)
+        sa, sb, sc, sd = (t[sl].cpu().numpy().copy() for t in (a, b, c, d))
+        sa[0] = 0.0
+        sc[-1] = 0.0
+        _check(xh[sl], sa, sb, sc, sd)
+    del a, b, c, d, x
+    torch.cuda.empty_cache()
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
@@ -361,9 +479,12 @@ def test_bench_row_sharded_path(world, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), str(root / "bench.py"),
            "--gpus", str(world), "--steps", "3", "--warmup", "3", "--rows-per-gpu", "333337",
-           "--dist-backend", "gloo", "--same-device", "--no-e2e", "--check"]
+           "--dist-backend", "gloo", "--same-device", "--e2e-steps", "2", "--check"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == world and line["check"]["rel_err"] <= REL_TOL
     assert line["check"]["residual"] <= RES_TOL
+    # the end-to-end path (DistributedSolver.solve_host from pinned host rows)
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 32 * 333337 * world
+    assert line["check"]["e2e"]["rel_err"] <= REL_TOL and line["check"]["e2e"]["residual"] <= RES_TOL
