@@ -21,6 +21,7 @@
  *                           runs on the GPU here instead of PAPER.md:63's CPU).
  *   pm_solve_batch_device_f64, pm_dist_*  <- B200 additions (BASELINE.json
  *                           configs 4 and 5).
+ *   *_f32                <- FP32 variants of the above.
  *   pm_recommend_streams <- streamtune::recommend.
  *
  * Conventions
@@ -188,6 +189,32 @@ int pm_dist_reduce_f64(pm_handle_t h, const double* a, const double* b, const do
 int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const double* c,
                       const double* d, double* x, int64_t n_local, int32_t m, int32_t rank,
                       int32_t world, const double* iface_all, void* stream);
+
+/* FP32 variants (the paper's FP32 experiments; Table 5 and
+ * streamtune::recommend_fp32): the same pipeline, plan, options and status
+ * codes on float arrays -- half the HBM and host-link bytes per unknown.
+ * The FP32 generator writes the round-to-nearest FP32 images of the FP64
+ * generator's values.  Accuracy is FP32's: see DESIGN.md (relative error vs
+ * the FP64 solution of the same FP32 inputs <= 1e-4 on the synthetic
+ * diagonally dominant systems). */
+int pm_solve_device_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                        const float* d, float* x, int64_t n, int32_t m, void* stream);
+int pm_solve_batch_device_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                              const float* d, float* x, int64_t n_per_system, int64_t batch,
+                              int32_t m, void* stream);
+int pm_solve_host_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                      const float* d, float* x, int64_t n, int32_t m, int32_t num_streams);
+int pm_generate_f32(pm_handle_t h, float* a, float* b, float* c, float* d, int64_t n,
+                    uint64_t seed, void* stream);
+int pm_generate_range_f32(pm_handle_t h, float* a, float* b, float* c, float* d,
+                          int64_t n_total, int64_t row0, int64_t count, uint64_t seed,
+                          void* stream);
+int pm_dist_reduce_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                       const float* d, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                       float* iface, void* stream);
+int pm_dist_solve_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                      const float* d, float* x, int64_t n_local, int32_t m, int32_t rank,
+                      int32_t world, const float* iface_all, void* stream);
 
 /* Diagnostics: number of kernel launches the last solve call enqueued, and
  * the level plan (rows per level) of the last plan. */

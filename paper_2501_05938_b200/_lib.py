@@ -58,6 +58,18 @@ PM_SIGNATURES = [
      [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),
     ("pm_generate_range_f64", C.c_int,
      [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_void_p]),
+    # FP32 variants (same signatures on float arrays)
+    ("pm_solve_device_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
+    ("pm_solve_batch_device_f32", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int64, C.c_int32, C.c_void_p]),
+    ("pm_solve_host_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32]),
+    ("pm_generate_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_uint64, C.c_void_p]),
+    ("pm_generate_range_f32", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_void_p]),
+    ("pm_dist_reduce_f32", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),
+    ("pm_dist_solve_f32", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),
     ("pm_last_launch_count", C.c_int, [C.c_void_p]),
     ("pm_kernel_times", C.c_int,
      [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int32]),

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -31,7 +32,6 @@
 
 namespace {
 
-using pm::TileArgs;
 
 struct Level {
   int64_t n = 0;
@@ -39,11 +39,11 @@ struct Level {
   int P = 128;
   int64_t T = 0;
   int64_t ntiles = 0;
-  const double* a = nullptr;
-  const double* b = nullptr;
-  const double* c = nullptr;
-  const double* d = nullptr;
-  double* x = nullptr;
+  const void* a = nullptr;  // arrays of the level's precision (Prec<R>::Real)
+  const void* b = nullptr;
+  const void* c = nullptr;
+  const void* d = nullptr;
+  void* x = nullptr;
   bool bulk = true;
   int pad_mode = 1;
   int stages = 2;
@@ -59,6 +59,57 @@ int choose_P(int m) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// The kernels of one precision: pm (FP64, the north_star solver) and pm32
+// (FP32, the paper's FP32 experiments).
+template <class R>
+struct Prec;
+template <>
+struct Prec<double> {
+  using Args = pm::TileArgs;
+  using Node = pm::Node;
+  static cudaError_t warp(int mode, const Args& a, int w, int sm, cudaStream_t st, int* g) {
+    return pm::launch_warp_tile_kernel(mode, a, w, sm, st, g);
+  }
+  static cudaError_t tile(int mode, const Args& a, int P, bool bulk, int sm, cudaStream_t st, int* g) {
+    return pm::launch_tile_kernel(mode, a, P, bulk, sm, st, g);
+  }
+  static int ctas(int mode, int m, int stages, int w, bool chain) {
+    return pm::warp_kernel_ctas_per_sm(mode, m, stages, w, chain);
+  }
+  static size_t tile_smem(int mode, int P, int m, int S) { return pm::tile_smem_bytes(mode, P, m, S); }
+  static size_t warp_smem(int mode, int m, int S) { return pm::warp_smem_bytes(mode, m, S); }
+  static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st) {
+    return pm::launch_dist_chain(ia, w, r, xb, f, st);
+  }
+  static cudaError_t generate(double* a, double* b, double* c, double* d, int64_t n, int64_t r0,
+                              int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
+    return pm::launch_generate(a, b, c, d, n, r0, cnt, seed, sm, st);
+  }
+};
+template <>
+struct Prec<float> {
+  using Args = pm32::TileArgs;
+  using Node = pm32::Node;
+  static cudaError_t warp(int mode, const Args& a, int w, int sm, cudaStream_t st, int* g) {
+    return pm32::launch_warp_tile_kernel(mode, a, w, sm, st, g);
+  }
+  static cudaError_t tile(int mode, const Args& a, int P, bool bulk, int sm, cudaStream_t st, int* g) {
+    return pm32::launch_tile_kernel(mode, a, P, bulk, sm, st, g);
+  }
+  static int ctas(int mode, int m, int stages, int w, bool chain) {
+    return pm32::warp_kernel_ctas_per_sm(mode, m, stages, w, chain);
+  }
+  static size_t tile_smem(int mode, int P, int m, int S) { return pm32::tile_smem_bytes(mode, P, m, S); }
+  static size_t warp_smem(int mode, int m, int S) { return pm32::warp_smem_bytes(mode, m, S); }
+  static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st) {
+    return pm32::launch_dist_chain(ia, w, r, xb, f, st);
+  }
+  static cudaError_t generate(float* a, float* b, float* c, float* d, int64_t n, int64_t r0,
+                              int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
+    return pm32::launch_generate(a, b, c, d, n, r0, cnt, seed, sm, st);
+  }
+};
 
 }  // namespace
 
@@ -83,11 +134,11 @@ struct pm_handle_s {
   int batch_force_stages = 0;
   pm::BatchPlan last_batch_plan{0, 0, 0, 0, 0, 0};
   // device scratch for upper levels (+ dist boundary values)
-  double* scratch = nullptr;
+  char* scratch = nullptr;  // level arrays of the current solve's precision
   size_t scratch_bytes = 0;
   int* dflag = nullptr;
   // device staging for the host path: a, b, c, d, x
-  double* hbuf = nullptr;
+  char* hbuf = nullptr;
   size_t hbuf_bytes = 0;
   std::vector<cudaStream_t> pool;
   cudaStream_t main = nullptr;
@@ -144,21 +195,23 @@ int ensure_scratch(pm_handle_t h, size_t bytes) {
   return PM_OK;
 }
 
+template <class R>
 int pick_stages(int want, int P, int m) {
   int S = std::max(1, std::min(want, 4));
-  while (S > 1 && pm::tile_smem_bytes(pm::kModeSolve, P, m, S) > kSmemLimit) --S;
+  while (S > 1 && Prec<R>::tile_smem(pm::kModeSolve, P, m, S) > kSmemLimit) --S;
   return S;
 }
 
 // Warp-tile configuration of a level: ring depth and as many warps per CTA
 // (<= PM_OPT_WARPS_PER_CTA) as the shared memory allows.
+template <class R>
 void set_warp_tiles(pm_handle_t h, Level& L) {
   int S = std::max(1, std::min(std::max(h->stages, h->solve_stages), 4));
   int W = 0;
   while (S >= 1) {
     W = (int)std::min<size_t>(h->warps_per_cta,
-                              kSmemLimit / pm::warp_smem_bytes(pm::kModeReduce, L.m, S));
-    W = (int)std::min<size_t>(W, kSmemLimit / pm::warp_smem_bytes(pm::kModeSolve, L.m, 1));
+                              kSmemLimit / Prec<R>::warp_smem(pm::kModeReduce, L.m, S));
+    W = (int)std::min<size_t>(W, kSmemLimit / Prec<R>::warp_smem(pm::kModeSolve, L.m, 1));
     if (W >= 1) break;
     --S;
   }
@@ -172,8 +225,9 @@ void set_warp_tiles(pm_handle_t h, Level& L) {
 // Builds h->levels for a level-0 system; allocates scratch for levels >= 1.
 // ragged0: the caller's last tile must not be padded (row-sharded ranks that
 // are not the last one); then m must divide n and upper levels use m = 2.
-int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b, const double* c,
-               const double* d, double* x, bool ragged0, size_t extra_doubles,
+template <class R>
+int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R* c,
+               const R* d, R* x, bool ragged0, size_t extra_elems,
                bool allow_chain = true, int nparts = 1) {
   std::vector<Level> lv;
   Level L0;
@@ -184,11 +238,11 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   L0.bulk = aligned16(a) && aligned16(b) && aligned16(c) && aligned16(d) && aligned16(x);
   // a system that fits one CTA tile is solved by a single ROOT launch
   const bool one_tile = n <= (int64_t)choose_P(m) * m;
-  if (L0.bulk && h->warp_tiles && !one_tile) set_warp_tiles(h, L0);
+  if (L0.bulk && h->warp_tiles && !one_tile) set_warp_tiles<R>(h, L0);
   if (L0.warps_per_cta == 0) {
     L0.P = choose_P(m);
-    L0.stages = pick_stages(h->stages, L0.P, m);
-    if (pm::tile_smem_bytes(pm::kModeSolve, L0.P, m, 1) > kSmemLimit)
+    L0.stages = pick_stages<R>(h->stages, L0.P, m);
+    if (Prec<R>::tile_smem(pm::kModeSolve, L0.P, m, 1) > kSmemLimit)
       return fail(h, PM_ERR_VALIDATION, "sub-system size m too large for shared memory");
   }
   L0.T = (int64_t)L0.P * m;
@@ -206,7 +260,7 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   h->part_chunks.clear();
   h->part_base.clear();
   if (h->chain) {
-    const int ctas = pm::warp_kernel_ctas_per_sm(pm::kModeSolve, m, std::max(1, std::min(h->solve_stages > 0 ? h->solve_stages : L0.stages, L0.stages)),
+    const int ctas = Prec<R>::ctas(pm::kModeSolve, m, std::max(1, std::min(h->solve_stages > 0 ? h->solve_stages : L0.stages, L0.stages)),
                                                  L0.warps_per_cta, true);
     int64_t C = (int64_t)std::max(1, ctas) * L0.warps_per_cta * h->sm_count;
     C = std::min<int64_t>(C, 8192);
@@ -247,18 +301,18 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
       U.m = h->root_m;
       if (U.n > (int64_t)128 * h->root_m && h->warp_tiles) {
         U.m = h->upper_m;
-        set_warp_tiles(h, U);
+        set_warp_tiles<R>(h, U);
       }
     } else {
       U.m = m_up;
     }
-    if (U.warps_per_cta == 0) U.stages = pick_stages(h->stages, U.P, U.m);
+    if (U.warps_per_cta == 0) U.stages = pick_stages<R>(h->stages, U.P, U.m);
     U.T = (int64_t)U.P * U.m;
     U.ntiles = (U.n + U.T - 1) / U.T;
     lv.push_back(U);
   }
   // scratch: levels >= 1 hold a, b, c, d, x (n_L each); 256-byte aligned
-  size_t total = extra_doubles;
+  size_t total = extra_elems;  // in elements of R
   std::vector<size_t> off(lv.size(), 0);
   for (size_t k = 1; k < lv.size(); ++k) {
     off[k] = total;
@@ -267,14 +321,15 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   size_t nodes_off = 0;
   if (h->chain) {
     nodes_off = (total + 31) / 32 * 32;
-    total = nodes_off + (size_t)L0.ntiles * 8;  // 7 doubles per Node, padded to 8
+    total = nodes_off + (size_t)L0.ntiles * 8;  // 7 reals per Node, padded to 8
   }
-  int st = ensure_scratch(h, total * sizeof(double));
+  int st = ensure_scratch(h, total * sizeof(R));
   if (st) return st;
-  h->chain_nodes = h->chain ? (void*)(h->scratch + nodes_off) : nullptr;
+  R* scr = reinterpret_cast<R*>(h->scratch);
+  h->chain_nodes = h->chain ? (void*)(scr + nodes_off) : nullptr;
   for (size_t k = 1; k < lv.size(); ++k) {
     const size_t stride = (size_t)((lv[k].n + 31) / 32 * 32);
-    double* base = h->scratch + off[k];
+    R* base = scr + off[k];
     lv[k].a = base;
     lv[k].b = base + stride;
     lv[k].c = base + 2 * stride;
@@ -286,9 +341,11 @@ int build_plan(pm_handle_t h, int64_t n, int m, const double* a, const double* b
   return PM_OK;
 }
 
-TileArgs args_for(pm_handle_t h, const Level& L, int64_t t0, int64_t t1) {
-  TileArgs A;
-  A.a = L.a; A.b = L.b; A.c = L.c; A.d = L.d; A.x = L.x;
+template <class R>
+typename Prec<R>::Args args_for(pm_handle_t h, const Level& L, int64_t t0, int64_t t1) {
+  typename Prec<R>::Args A;
+  A.a = static_cast<const R*>(L.a); A.b = static_cast<const R*>(L.b);
+  A.c = static_cast<const R*>(L.c); A.d = static_cast<const R*>(L.d); A.x = static_cast<R*>(L.x);
   A.n = L.n;
   A.tile_begin = t0;
   A.tile_end = t1;
@@ -310,7 +367,8 @@ cudaEvent_t next_kevent(pm_handle_t h) {
   return h->kev[k - 2];
 }
 
-int launch(pm_handle_t h, int mode, const TileArgs& A, const Level& L, cudaStream_t st) {
+template <class R>
+int launch(pm_handle_t h, int mode, const typename Prec<R>::Args& A, const Level& L, cudaStream_t st) {
   int grid = 0;
   const int level = (int)(&L - h->levels.data());
   const bool timed = h->ktimes && next_kevent(h) != nullptr;
@@ -318,9 +376,9 @@ int launch(pm_handle_t h, int mode, const TileArgs& A, const Level& L, cudaStrea
   if (timed) cudaEventRecord(h->kev[ev], st);
   cudaError_t e;
   if (L.warps_per_cta > 0 && mode != pm::kModeRoot)
-    e = pm::launch_warp_tile_kernel(mode, A, L.warps_per_cta, h->sm_count, st, &grid);
+    e = Prec<R>::warp(mode, A, L.warps_per_cta, h->sm_count, st, &grid);
   else
-    e = pm::launch_tile_kernel(mode, A, L.P, L.bulk, h->sm_count, st, &grid);
+    e = Prec<R>::tile(mode, A, L.P, L.bulk, h->sm_count, st, &grid);
   if (e != cudaSuccess) return cuda_fail(h, e, "tile kernel launch");
   if (timed) {
     cudaEventRecord(h->kev[ev + 1], st);
@@ -332,72 +390,78 @@ int launch(pm_handle_t h, int mode, const TileArgs& A, const Level& L, cudaStrea
 
 
 // REDUCE of level k over tiles [t0, t1): writes rows into level k+1 (or `out4`).
-void set_chain(pm_handle_t h, TileArgs& A, int part) {
+template <class R>
+void set_chain(pm_handle_t h, typename Prec<R>::Args& A, int part) {
   A.nchunks = h->part_chunks[part];
   A.chunk_base = h->part_base[part];
-  A.chain_nodes = static_cast<pm::Node*>(h->chain_nodes);
+  A.chain_nodes = static_cast<typename Prec<R>::Node*>(h->chain_nodes);
 }
 
+template <class R>
 int enq_reduce(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, bool zf, bool zl,
-               int64_t sys_len, double* const* out4, int part = 0) {
+               int64_t sys_len, R* const* out4, int part = 0) {
   const Level& L = h->levels[k];
-  TileArgs A = args_for(h, L, t0, t1);
+  typename Prec<R>::Args A = args_for<R>(h, L, t0, t1);
   if (out4) {
     A.ra = out4[0]; A.rb = out4[1]; A.rc = out4[2]; A.rd = out4[3];
   } else {
     const Level& U = h->levels[k + 1];
-    A.ra = const_cast<double*>(U.a); A.rb = const_cast<double*>(U.b);
-    A.rc = const_cast<double*>(U.c); A.rd = const_cast<double*>(U.d);
+    A.ra = static_cast<R*>(const_cast<void*>(U.a)); A.rb = static_cast<R*>(const_cast<void*>(U.b));
+    A.rc = static_cast<R*>(const_cast<void*>(U.c)); A.rd = static_cast<R*>(const_cast<void*>(U.d));
   }
   A.zero_first = zf;
   A.zero_last = zl;
   A.sys_len = (k == 0) ? sys_len : 0;
-  if (k == 0 && h->chain) set_chain(h, A, part);
-  return launch(h, pm::kModeReduce, A, L, st);
+  if (k == 0 && h->chain) set_chain<R>(h, A, part);
+  return launch<R>(h, pm::kModeReduce, A, L, st);
 }
 
+template <class R>
 int enq_solve(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, bool zf, bool zl,
-              int64_t sys_len, const double* xb, int part = 0) {
+              int64_t sys_len, const R* xb, int part = 0) {
   const Level& L = h->levels[k];
-  TileArgs A = args_for(h, L, t0, t1);
-  A.xb = xb ? xb : h->levels[k + 1].x;
+  typename Prec<R>::Args A = args_for<R>(h, L, t0, t1);
+  A.xb = xb ? xb : static_cast<const R*>(h->levels[k + 1].x);
   if (L.warps_per_cta > 0 && h->solve_stages > 0) A.stages = std::min(h->solve_stages, L.stages);
   A.zero_first = zf;
   A.zero_last = zl;
   A.sys_len = (k == 0) ? sys_len : 0;
   A.reverse = h->reverse;
-  if (k == 0 && h->chain) set_chain(h, A, part);
-  return launch(h, pm::kModeSolve, A, L, st);
+  if (k == 0 && h->chain) set_chain<R>(h, A, part);
+  return launch<R>(h, pm::kModeSolve, A, L, st);
 }
 
+template <class R>
 int enq_root(pm_handle_t h, size_t k, cudaStream_t st, int64_t sys_len) {
   const Level& L = h->levels[k];
-  TileArgs A = args_for(h, L, 0, 1);
+  typename Prec<R>::Args A = args_for<R>(h, L, 0, 1);
   A.sys_len = (k == 0) ? sys_len : 0;
-  return launch(h, pm::kModeRoot, A, L, st);
+  return launch<R>(h, pm::kModeRoot, A, L, st);
 }
 
 
 // Upper levels (1..top) on one stream: REDUCE 1..top-1, ROOT top, SOLVE
 // top-1..1 (chain mode: level 1 is the top, a single ROOT).
+template <class R>
 int enq_upper(pm_handle_t h, cudaStream_t st) {
   const size_t top = h->levels.size() - 1;
   int r;
   for (size_t k = 1; k < top; ++k)
-    if ((r = enq_reduce(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
-  if (top >= 1 && (r = enq_root(h, top, st, 0))) return r;
+    if ((r = enq_reduce<R>(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
+  if (top >= 1 && (r = enq_root<R>(h, top, st, 0))) return r;
   for (size_t k = top; k-- > 1;)
-    if ((r = enq_solve(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
+    if ((r = enq_solve<R>(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
   return PM_OK;
 }
 
 // Whole solve of the planned system on one stream.
+template <class R>
 int enq_full(pm_handle_t h, cudaStream_t st, int64_t sys_len) {
   int r;
-  if (h->levels.size() == 1) return enq_root(h, 0, st, sys_len);
-  if ((r = enq_reduce(h, 0, 0, h->levels[0].ntiles, st, true, true, sys_len, nullptr))) return r;
-  if ((r = enq_upper(h, st))) return r;
-  return enq_solve(h, 0, 0, h->levels[0].ntiles, st, true, true, sys_len, nullptr);
+  if (h->levels.size() == 1) return enq_root<R>(h, 0, st, sys_len);
+  if ((r = enq_reduce<R>(h, 0, 0, h->levels[0].ntiles, st, true, true, sys_len, nullptr))) return r;
+  if ((r = enq_upper<R>(h, st))) return r;
+  return enq_solve<R>(h, 0, 0, h->levels[0].ntiles, st, true, true, sys_len, nullptr);
 }
 
 int validate_common(pm_handle_t h, const void* a, const void* b, const void* c, const void* d,
@@ -446,6 +510,309 @@ int read_flag(pm_handle_t h, cudaStream_t st) {
 }
 
 }  // namespace
+
+// ---- the solver entry points, one instantiation per precision -------------
+
+template <class R>
+int solve_device_impl(pm_handle_t h, const R* a, const R* b, const R* c,
+                        const R* d, R* x, int64_t n, int32_t m, void* stream) {
+  int r = validate_common(h, a, b, c, d, x, n, m);
+  if (r) return r;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  if ((r = build_plan<R>(h, n, m, a, b, c, d, x, false, 0))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  return enq_full<R>(h, st, 0);
+}
+
+template <class R>
+int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
+                              const R* d, R* x, int64_t n_per_system, int64_t batch,
+                              int32_t m, void* stream) {
+  if (batch < 1) return fail(h, PM_ERR_VALIDATION, "batch must be at least 1");
+  if (n_per_system < 1) return fail(h, PM_ERR_VALIDATION, "SLAE size must be at least 1");
+  if (n_per_system > INT64_MAX / batch) return fail(h, PM_ERR_VALIDATION, "batch too large");
+  const int64_t n = n_per_system * batch;
+  int r = validate_common(h, a, b, c, d, x, n, m);
+  if (r) return r;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  pm::BatchPlan pl{};
+  if (std::is_same<R, double>::value && batch > 1 && h->batch_cluster && aligned16(a) && aligned16(b) && aligned16(c) &&
+      aligned16(d) && aligned16(x) &&
+      pm::plan_batch(m, n_per_system, batch, h->sm_count, (int64_t)h->batch_l2_mb << 20,
+                     h->batch_force_cluster, h->batch_force_warps, h->batch_force_stages, &pl)) {
+    pm::BatchArgs A;  // the cluster kernel is FP64-only
+    A.a = reinterpret_cast<const double*>(a); A.b = reinterpret_cast<const double*>(b);
+    A.c = reinterpret_cast<const double*>(c); A.d = reinterpret_cast<const double*>(d);
+    A.x = reinterpret_cast<double*>(x);
+    A.n_sys = n_per_system;
+    A.batch = batch;
+    A.flag = h->dflag;
+    h->levels.clear();
+    h->last_batch_plan = pl;
+    const bool timed = h->ktimes && next_kevent(h) != nullptr;
+    const size_t ev = h->krec.size() * 2;
+    if (timed) cudaEventRecord(h->kev[ev], st);
+    PM_CUDA(h, pm::launch_batch_cluster(m, A, pl, st));
+    if (timed) {
+      cudaEventRecord(h->kev[ev + 1], st);
+      h->krec.push_back({4, 0, ev});
+    }
+    ++h->launches;
+    return PM_OK;
+  }
+  h->last_batch_plan = pm::BatchPlan{0, 0, 0, 0, 0, 0};
+  if ((r = build_plan<R>(h, n, m, a, b, c, d, x, false, 0))) return r;
+  return enq_full<R>(h, st, batch > 1 ? n_per_system : 0);
+}
+
+template <class R>
+int solve_host_impl(pm_handle_t h, const R* a, const R* b, const R* c,
+                      const R* d, R* x, int64_t n, int32_t m, int32_t num_streams) {
+  int r = validate_common(h, a, b, c, d, x, n, m);
+  if (r) return r;
+  if (num_streams != 0 && !streamtune::StreamCount::is_valid(num_streams))
+    return fail(h, PM_ERR_VALIDATION,
+                streamtune::InvalidStreamCountError(num_streams).what());
+  PM_CUDA(h, cudaSetDevice(h->device));
+  int ns = num_streams;
+  if (ns == 0) {
+    try {
+      ns = streamtune::recommend(h->bundle, (uint64_t)n).chosen.value();
+    } catch (const std::exception& ex) {
+      return fail(h, PM_ERR_VALIDATION, ex.what());
+    }
+  }
+  // device staging: a, b, c, d, x (x separate so the caller may alias d)
+  const size_t stride = (size_t)((n + 31) / 32 * 32);
+  const size_t need = 5 * stride * sizeof(R);
+  if (need > h->hbuf_bytes) {
+    if (h->hbuf) {
+      PM_CUDA(h, cudaDeviceSynchronize());
+      PM_CUDA(h, cudaFree(h->hbuf));
+      h->hbuf = nullptr;
+      h->hbuf_bytes = 0;
+    }
+    PM_CUDA(h, cudaMalloc(&h->hbuf, need));
+    h->hbuf_bytes = need;
+  }
+  R* da = reinterpret_cast<R*>(h->hbuf);
+  R* db = da + stride;
+  R* dc = db + stride;
+  R* dd = dc + stride;
+  R* dx = dd + stride;
+  h->launches = 0;
+  {
+    // parts = the stream chunks, so that chain chunks never straddle them
+    const int parts_hint = ns > 1 ? ns : 1;
+    if ((r = build_plan<R>(h, n, m, da, db, dc, dd, dx, false, 0, true, parts_hint))) return r;
+  }
+  const Level& L0 = h->levels[0];
+  const bool single_tile = h->levels.size() == 1;
+  int chunks = single_tile ? 1 : h->nparts;
+
+  cudaStream_t main = h->main;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> evs;
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (h->stream_mode == 1)
+      for (cudaStream_t s : streams) cudaStreamDestroy(s);
+  };
+  cudaEvent_t tev[6];
+  for (int k = 0; k < 6; ++k) {
+    cudaError_t e = cudaEventCreate(&tev[k]);
+    if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaEventCreate"); }
+    evs.push_back(tev[k]);
+  }
+  // The stream set: created inside the timed region in stream mode 1 (the
+  // paper's T_overhead includes creating them, PAPER.md:73-74, 85-86).
+  cudaEventRecord(tev[0], main);
+  if (ns > 1) {
+    if (h->stream_mode == 1) {
+      for (int k = 0; k < ns; ++k) {
+        cudaStream_t s;
+        cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaStreamCreate"); }
+        streams.push_back(s);
+      }
+    } else {
+      while ((int)h->pool.size() < ns) {
+        cudaStream_t s;
+        cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaStreamCreate"); }
+        h->pool.push_back(s);
+      }
+      streams.assign(h->pool.begin(), h->pool.begin() + ns);
+    }
+  }
+  const bool record = h->timings && ns == 1;
+  auto bytes_of = [](int64_t rows) { return (size_t)rows * sizeof(R); };
+  cudaError_t e = cudaSuccess;
+  auto h2d = [&](int64_t r0, int64_t r1, cudaStream_t s) {
+    const size_t bytes = bytes_of(r1 - r0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(da + r0, a + r0, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db + r0, b + r0, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dc + r0, c + r0, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dd + r0, d + r0, bytes, cudaMemcpyHostToDevice, s);
+  };
+  auto d2h = [&](int64_t r0, int64_t r1, cudaStream_t s) {
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(x + r0, dx + r0, bytes_of(r1 - r0), cudaMemcpyDeviceToHost, s);
+  };
+
+  if (ns == 1 || chunks <= 1) {
+    h2d(0, n, main);
+    if (record) cudaEventRecord(tev[1], main);
+    if (single_tile) {
+      if (e == cudaSuccess && (r = enq_root<R>(h, 0, main, 0))) { cleanup(); return r; }
+      if (record) { cudaEventRecord(tev[2], main); cudaEventRecord(tev[3], main); }
+    } else {
+      if (e == cudaSuccess && (r = enq_reduce<R>(h, 0, 0, L0.ntiles, main, true, true, 0, nullptr))) { cleanup(); return r; }
+      if (record) cudaEventRecord(tev[2], main);
+      if (e == cudaSuccess && (r = enq_upper<R>(h, main))) { cleanup(); return r; }
+      if (record) cudaEventRecord(tev[3], main);
+      if (e == cudaSuccess && (r = enq_solve<R>(h, 0, 0, L0.ntiles, main, true, true, 0, nullptr))) { cleanup(); return r; }
+    }
+    if (record) cudaEventRecord(tev[4], main);
+    d2h(0, n, main);
+  } else {
+    // fork
+    cudaEvent_t fork, join;
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    evs.push_back(fork);
+    evs.push_back(join);
+    std::vector<cudaEvent_t> done(chunks);
+    for (int k = 0; k < chunks; ++k) {
+      cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+      evs.push_back(done[k]);
+    }
+    cudaEventRecord(fork, main);
+    for (int k = 0; k < chunks; ++k) {
+      const int64_t t0 = L0.ntiles * k / chunks, t1 = L0.ntiles * (k + 1) / chunks;
+      const int64_t r0 = t0 * L0.T, r1 = std::min(n, t1 * L0.T);
+      cudaStream_t s = streams[k];
+      cudaStreamWaitEvent(s, fork, 0);
+      h2d(r0, r1, s);
+      if (e == cudaSuccess && (r = enq_reduce<R>(h, 0, t0, t1, s, true, true, 0, nullptr, k))) { cleanup(); return r; }
+      cudaEventRecord(done[k], s);
+    }
+    for (int k = 0; k < chunks; ++k) cudaStreamWaitEvent(main, done[k], 0);
+    if (e == cudaSuccess && (r = enq_upper<R>(h, main))) { cleanup(); return r; }
+    cudaEventRecord(join, main);
+    for (int k = 0; k < chunks; ++k) {
+      const int64_t t0 = L0.ntiles * k / chunks, t1 = L0.ntiles * (k + 1) / chunks;
+      const int64_t r0 = t0 * L0.T, r1 = std::min(n, t1 * L0.T);
+      cudaStream_t s = streams[k];
+      cudaStreamWaitEvent(s, join, 0);
+      if (e == cudaSuccess && (r = enq_solve<R>(h, 0, t0, t1, s, true, true, 0, nullptr, k))) { cleanup(); return r; }
+      d2h(r0, r1, s);
+      cudaEventRecord(done[k], s);
+    }
+    for (int k = 0; k < chunks; ++k) cudaStreamWaitEvent(main, done[k], 0);
+  }
+  if (h->stream_mode == 1) {
+    for (cudaStream_t s : streams) cudaStreamDestroy(s);
+    streams.clear();
+  }
+  cudaEventRecord(tev[5], main);
+  if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaMemcpyAsync"); }
+  cudaError_t se = cudaEventSynchronize(tev[5]);
+  if (se != cudaSuccess) { cleanup(); return cuda_fail(h, se, "solve"); }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, tev[0], tev[5]);
+  h->last_total_ms = ms;
+  h->last_streams = ns;
+  std::memset(&h->last_t, 0, sizeof(h->last_t));
+  h->last_t.slae_size = (uint64_t)n;
+  if (record) {
+    float t[5];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], tev[k], tev[k + 1]);
+    h->last_t.t1_h2d = t[0];
+    h->last_t.t1_comp = t[1];
+    h->last_t.t2_comp = t[2];
+    h->last_t.t3_comp = t[3];
+    h->last_t.t3_d2h = t[4];
+  }
+  cleanup();
+  h->last_stream = main;
+  return read_flag(h, main);
+}
+
+template <class R>
+int generate_range_impl(pm_handle_t h, R* a, R* b, R* c, R* d,
+                          int64_t n_total, int64_t row0, int64_t count, uint64_t seed,
+                          void* stream) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (n_total < 1 || count < 1 || row0 < 0 || row0 + count > n_total)
+    return fail(h, PM_ERR_VALIDATION, "row range outside [0, n_total)");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PM_CUDA(h, Prec<R>::generate(a, b, c, d, n_total, row0, count, seed, h->sm_count, st));
+  h->last_stream = st;
+  return PM_OK;
+}
+
+template <class R>
+int dist_reduce_impl(pm_handle_t h, const R* a, const R* b, const R* c,
+                       const R* d, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                       R* iface, void* stream) {
+  // x is not used by the reduce; pass d so the plan's alignment test sees a real pointer
+  int r = validate_common(h, a, b, c, d, d, n_local, m);
+  if (r) return r;
+  if (!iface) return fail(h, PM_ERR_VALIDATION, "null iface pointer");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  const bool last = rank == world - 1;
+  if (!last && n_local % m != 0)
+    return fail(h, PM_ERR_VALIDATION, "n_local must be a multiple of m on every rank but the last");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  // same plan (and the same 32-R prefix) as pm_dist_solve_f64
+  if ((r = build_plan<R>(h, n_local, m, a, b, c, d, const_cast<R*>(d), !last, 32, false))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  const bool zf = rank == 0, zl = last;
+  const size_t top = h->levels.size() - 1;
+  for (size_t k = 0; k < top; ++k)
+    if ((r = enq_reduce<R>(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
+  R* out4[4] = {iface, iface + 2, iface + 4, iface + 6};
+  return enq_reduce<R>(h, top, 0, 1, st, zf, zl, 0, out4);
+}
+
+template <class R>
+int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
+                      const R* d, R* x, int64_t n_local, int32_t m, int32_t rank,
+                      int32_t world, const R* iface_all, void* stream) {
+  int r = validate_common(h, a, b, c, d, x, n_local, m);
+  if (r) return r;
+  if (!iface_all) return fail(h, PM_ERR_VALIDATION, "null iface_all pointer");
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  const bool last = rank == world - 1;
+  if (!last && n_local % m != 0)
+    return fail(h, PM_ERR_VALIDATION, "n_local must be a multiple of m on every rank but the last");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  h->launches = 0;
+  // two extra doubles in front of the level scratch hold this rank's (xf, xl)
+  if ((r = build_plan<R>(h, n_local, m, a, b, c, d, x, !last, 32, false))) return r;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->last_stream = st;
+  R* xb = reinterpret_cast<R*>(h->scratch);  // extra_elems region
+  PM_CUDA(h, Prec<R>::dist_chain(iface_all, world, rank, xb, h->dflag, st));
+  ++h->launches;
+  const bool zf = rank == 0, zl = last;
+  const size_t top = h->levels.size() - 1;
+  if ((r = enq_solve<R>(h, top, 0, 1, st, zf, zl, 0, xb))) return r;
+  for (size_t k = top; k-- > 0;)
+    if ((r = enq_solve<R>(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
+  return PM_OK;
+}
 
 extern "C" {
 
@@ -515,6 +882,7 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       return PM_OK;
     case PM_OPT_PDL:
       pm::set_pdl(value != 0);
+      pm32::set_pdl(value != 0);
       return PM_OK;
     case PM_OPT_CHAIN:
       h->opt_chain = value ? 1 : 0;
@@ -563,55 +931,22 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
 
 int pm_solve_device_f64(pm_handle_t h, const double* a, const double* b, const double* c,
                         const double* d, double* x, int64_t n, int32_t m, void* stream) {
-  int r = validate_common(h, a, b, c, d, x, n, m);
-  if (r) return r;
-  PM_CUDA(h, cudaSetDevice(h->device));
-  h->launches = 0;
-  if ((r = build_plan(h, n, m, a, b, c, d, x, false, 0))) return r;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  h->last_stream = st;
-  return enq_full(h, st, 0);
+  return solve_device_impl<double>(h, a, b, c, d, x, n, m, stream);
+}
+int pm_solve_device_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                        const float* d, float* x, int64_t n, int32_t m, void* stream) {
+  return solve_device_impl<float>(h, a, b, c, d, x, n, m, stream);
 }
 
 int pm_solve_batch_device_f64(pm_handle_t h, const double* a, const double* b, const double* c,
                               const double* d, double* x, int64_t n_per_system, int64_t batch,
                               int32_t m, void* stream) {
-  if (batch < 1) return fail(h, PM_ERR_VALIDATION, "batch must be at least 1");
-  if (n_per_system < 1) return fail(h, PM_ERR_VALIDATION, "SLAE size must be at least 1");
-  if (n_per_system > INT64_MAX / batch) return fail(h, PM_ERR_VALIDATION, "batch too large");
-  const int64_t n = n_per_system * batch;
-  int r = validate_common(h, a, b, c, d, x, n, m);
-  if (r) return r;
-  PM_CUDA(h, cudaSetDevice(h->device));
-  h->launches = 0;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  h->last_stream = st;
-  pm::BatchPlan pl{};
-  if (batch > 1 && h->batch_cluster && aligned16(a) && aligned16(b) && aligned16(c) &&
-      aligned16(d) && aligned16(x) &&
-      pm::plan_batch(m, n_per_system, batch, h->sm_count, (int64_t)h->batch_l2_mb << 20,
-                     h->batch_force_cluster, h->batch_force_warps, h->batch_force_stages, &pl)) {
-    pm::BatchArgs A;
-    A.a = a; A.b = b; A.c = c; A.d = d; A.x = x;
-    A.n_sys = n_per_system;
-    A.batch = batch;
-    A.flag = h->dflag;
-    h->levels.clear();
-    h->last_batch_plan = pl;
-    const bool timed = h->ktimes && next_kevent(h) != nullptr;
-    const size_t ev = h->krec.size() * 2;
-    if (timed) cudaEventRecord(h->kev[ev], st);
-    PM_CUDA(h, pm::launch_batch_cluster(m, A, pl, st));
-    if (timed) {
-      cudaEventRecord(h->kev[ev + 1], st);
-      h->krec.push_back({4, 0, ev});
-    }
-    ++h->launches;
-    return PM_OK;
-  }
-  h->last_batch_plan = pm::BatchPlan{0, 0, 0, 0, 0, 0};
-  if ((r = build_plan(h, n, m, a, b, c, d, x, false, 0))) return r;
-  return enq_full(h, st, batch > 1 ? n_per_system : 0);
+  return solve_batch_impl<double>(h, a, b, c, d, x, n_per_system, batch, m, stream);
+}
+int pm_solve_batch_device_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                              const float* d, float* x, int64_t n_per_system, int64_t batch,
+                              int32_t m, void* stream) {
+  return solve_batch_impl<float>(h, a, b, c, d, x, n_per_system, batch, m, stream);
 }
 
 int pm_last_batch_plan(pm_handle_t h, int32_t* out6) {
@@ -633,175 +968,11 @@ int pm_check(pm_handle_t h) {
 
 int pm_solve_host_f64(pm_handle_t h, const double* a, const double* b, const double* c,
                       const double* d, double* x, int64_t n, int32_t m, int32_t num_streams) {
-  int r = validate_common(h, a, b, c, d, x, n, m);
-  if (r) return r;
-  if (num_streams != 0 && !streamtune::StreamCount::is_valid(num_streams))
-    return fail(h, PM_ERR_VALIDATION,
-                streamtune::InvalidStreamCountError(num_streams).what());
-  PM_CUDA(h, cudaSetDevice(h->device));
-  int ns = num_streams;
-  if (ns == 0) {
-    try {
-      ns = streamtune::recommend(h->bundle, (uint64_t)n).chosen.value();
-    } catch (const std::exception& ex) {
-      return fail(h, PM_ERR_VALIDATION, ex.what());
-    }
-  }
-  // device staging: a, b, c, d, x (x separate so the caller may alias d)
-  const size_t stride = (size_t)((n + 31) / 32 * 32);
-  const size_t need = 5 * stride * sizeof(double);
-  if (need > h->hbuf_bytes) {
-    if (h->hbuf) {
-      PM_CUDA(h, cudaDeviceSynchronize());
-      PM_CUDA(h, cudaFree(h->hbuf));
-      h->hbuf = nullptr;
-      h->hbuf_bytes = 0;
-    }
-    PM_CUDA(h, cudaMalloc(&h->hbuf, need));
-    h->hbuf_bytes = need;
-  }
-  double* da = h->hbuf;
-  double* db = da + stride;
-  double* dc = db + stride;
-  double* dd = dc + stride;
-  double* dx = dd + stride;
-  h->launches = 0;
-  {
-    // parts = the stream chunks, so that chain chunks never straddle them
-    const int parts_hint = ns > 1 ? ns : 1;
-    if ((r = build_plan(h, n, m, da, db, dc, dd, dx, false, 0, true, parts_hint))) return r;
-  }
-  const Level& L0 = h->levels[0];
-  const bool single_tile = h->levels.size() == 1;
-  int chunks = single_tile ? 1 : h->nparts;
-
-  cudaStream_t main = h->main;
-  std::vector<cudaStream_t> streams;
-  std::vector<cudaEvent_t> evs;
-  auto cleanup = [&]() {
-    for (cudaEvent_t e : evs) cudaEventDestroy(e);
-    if (h->stream_mode == 1)
-      for (cudaStream_t s : streams) cudaStreamDestroy(s);
-  };
-  cudaEvent_t tev[6];
-  for (int k = 0; k < 6; ++k) {
-    cudaError_t e = cudaEventCreate(&tev[k]);
-    if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaEventCreate"); }
-    evs.push_back(tev[k]);
-  }
-  // The stream set: created inside the timed region in stream mode 1 (the
-  // paper's T_overhead includes creating them, PAPER.md:73-74, 85-86).
-  cudaEventRecord(tev[0], main);
-  if (ns > 1) {
-    if (h->stream_mode == 1) {
-      for (int k = 0; k < ns; ++k) {
-        cudaStream_t s;
-        cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-        if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaStreamCreate"); }
-        streams.push_back(s);
-      }
-    } else {
-      while ((int)h->pool.size() < ns) {
-        cudaStream_t s;
-        cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-        if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaStreamCreate"); }
-        h->pool.push_back(s);
-      }
-      streams.assign(h->pool.begin(), h->pool.begin() + ns);
-    }
-  }
-  const bool record = h->timings && ns == 1;
-  auto bytes_of = [](int64_t rows) { return (size_t)rows * sizeof(double); };
-  cudaError_t e = cudaSuccess;
-  auto h2d = [&](int64_t r0, int64_t r1, cudaStream_t s) {
-    const size_t bytes = bytes_of(r1 - r0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(da + r0, a + r0, bytes, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(db + r0, b + r0, bytes, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dc + r0, c + r0, bytes, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dd + r0, d + r0, bytes, cudaMemcpyHostToDevice, s);
-  };
-  auto d2h = [&](int64_t r0, int64_t r1, cudaStream_t s) {
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(x + r0, dx + r0, bytes_of(r1 - r0), cudaMemcpyDeviceToHost, s);
-  };
-
-  if (ns == 1 || chunks <= 1) {
-    h2d(0, n, main);
-    if (record) cudaEventRecord(tev[1], main);
-    if (single_tile) {
-      if (e == cudaSuccess && (r = enq_root(h, 0, main, 0))) { cleanup(); return r; }
-      if (record) { cudaEventRecord(tev[2], main); cudaEventRecord(tev[3], main); }
-    } else {
-      if (e == cudaSuccess && (r = enq_reduce(h, 0, 0, L0.ntiles, main, true, true, 0, nullptr))) { cleanup(); return r; }
-      if (record) cudaEventRecord(tev[2], main);
-      if (e == cudaSuccess && (r = enq_upper(h, main))) { cleanup(); return r; }
-      if (record) cudaEventRecord(tev[3], main);
-      if (e == cudaSuccess && (r = enq_solve(h, 0, 0, L0.ntiles, main, true, true, 0, nullptr))) { cleanup(); return r; }
-    }
-    if (record) cudaEventRecord(tev[4], main);
-    d2h(0, n, main);
-  } else {
-    // fork
-    cudaEvent_t fork, join;
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
-    evs.push_back(fork);
-    evs.push_back(join);
-    std::vector<cudaEvent_t> done(chunks);
-    for (int k = 0; k < chunks; ++k) {
-      cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
-      evs.push_back(done[k]);
-    }
-    cudaEventRecord(fork, main);
-    for (int k = 0; k < chunks; ++k) {
-      const int64_t t0 = L0.ntiles * k / chunks, t1 = L0.ntiles * (k + 1) / chunks;
-      const int64_t r0 = t0 * L0.T, r1 = std::min(n, t1 * L0.T);
-      cudaStream_t s = streams[k];
-      cudaStreamWaitEvent(s, fork, 0);
-      h2d(r0, r1, s);
-      if (e == cudaSuccess && (r = enq_reduce(h, 0, t0, t1, s, true, true, 0, nullptr, k))) { cleanup(); return r; }
-      cudaEventRecord(done[k], s);
-    }
-    for (int k = 0; k < chunks; ++k) cudaStreamWaitEvent(main, done[k], 0);
-    if (e == cudaSuccess && (r = enq_upper(h, main))) { cleanup(); return r; }
-    cudaEventRecord(join, main);
-    for (int k = 0; k < chunks; ++k) {
-      const int64_t t0 = L0.ntiles * k / chunks, t1 = L0.ntiles * (k + 1) / chunks;
-      const int64_t r0 = t0 * L0.T, r1 = std::min(n, t1 * L0.T);
-      cudaStream_t s = streams[k];
-      cudaStreamWaitEvent(s, join, 0);
-      if (e == cudaSuccess && (r = enq_solve(h, 0, t0, t1, s, true, true, 0, nullptr, k))) { cleanup(); return r; }
-      d2h(r0, r1, s);
-      cudaEventRecord(done[k], s);
-    }
-    for (int k = 0; k < chunks; ++k) cudaStreamWaitEvent(main, done[k], 0);
-  }
-  if (h->stream_mode == 1) {
-    for (cudaStream_t s : streams) cudaStreamDestroy(s);
-    streams.clear();
-  }
-  cudaEventRecord(tev[5], main);
-  if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaMemcpyAsync"); }
-  cudaError_t se = cudaEventSynchronize(tev[5]);
-  if (se != cudaSuccess) { cleanup(); return cuda_fail(h, se, "solve"); }
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, tev[0], tev[5]);
-  h->last_total_ms = ms;
-  h->last_streams = ns;
-  std::memset(&h->last_t, 0, sizeof(h->last_t));
-  h->last_t.slae_size = (uint64_t)n;
-  if (record) {
-    float t[5];
-    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], tev[k], tev[k + 1]);
-    h->last_t.t1_h2d = t[0];
-    h->last_t.t1_comp = t[1];
-    h->last_t.t2_comp = t[2];
-    h->last_t.t3_comp = t[3];
-    h->last_t.t3_d2h = t[4];
-  }
-  cleanup();
-  h->last_stream = main;
-  return read_flag(h, main);
+  return solve_host_impl<double>(h, a, b, c, d, x, n, m, num_streams);
+}
+int pm_solve_host_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                      const float* d, float* x, int64_t n, int32_t m, int32_t num_streams) {
+  return solve_host_impl<float>(h, a, b, c, d, x, n, m, num_streams);
 }
 
 int pm_last_stage_timings(pm_handle_t h, pm_stage_timings* out, double* total_ms,
@@ -867,72 +1038,42 @@ int pm_generate_f64(pm_handle_t h, double* a, double* b, double* c, double* d, i
                     uint64_t seed, void* stream) {
   return pm_generate_range_f64(h, a, b, c, d, n, 0, n, seed, stream);
 }
+int pm_generate_f32(pm_handle_t h, float* a, float* b, float* c, float* d, int64_t n,
+                    uint64_t seed, void* stream) {
+  return pm_generate_range_f32(h, a, b, c, d, n, 0, n, seed, stream);
+}
 
 int pm_generate_range_f64(pm_handle_t h, double* a, double* b, double* c, double* d,
                           int64_t n_total, int64_t row0, int64_t count, uint64_t seed,
                           void* stream) {
-  if (!h) return PM_ERR_VALIDATION;
-  if (n_total < 1 || count < 1 || row0 < 0 || row0 + count > n_total)
-    return fail(h, PM_ERR_VALIDATION, "row range outside [0, n_total)");
-  PM_CUDA(h, cudaSetDevice(h->device));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  PM_CUDA(h, pm::launch_generate(a, b, c, d, n_total, row0, count, seed, h->sm_count, st));
-  h->last_stream = st;
-  return PM_OK;
+  return generate_range_impl<double>(h, a, b, c, d, n_total, row0, count, seed, stream);
+}
+int pm_generate_range_f32(pm_handle_t h, float* a, float* b, float* c, float* d,
+                          int64_t n_total, int64_t row0, int64_t count, uint64_t seed,
+                          void* stream) {
+  return generate_range_impl<float>(h, a, b, c, d, n_total, row0, count, seed, stream);
 }
 
 int pm_dist_reduce_f64(pm_handle_t h, const double* a, const double* b, const double* c,
                        const double* d, int64_t n_local, int32_t m, int32_t rank, int32_t world,
                        double* iface, void* stream) {
-  // x is not used by the reduce; pass d so the plan's alignment test sees a real pointer
-  int r = validate_common(h, a, b, c, d, d, n_local, m);
-  if (r) return r;
-  if (!iface) return fail(h, PM_ERR_VALIDATION, "null iface pointer");
-  if (world < 1 || rank < 0 || rank >= world)
-    return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
-  const bool last = rank == world - 1;
-  if (!last && n_local % m != 0)
-    return fail(h, PM_ERR_VALIDATION, "n_local must be a multiple of m on every rank but the last");
-  PM_CUDA(h, cudaSetDevice(h->device));
-  h->launches = 0;
-  // same plan (and the same 32-double prefix) as pm_dist_solve_f64
-  if ((r = build_plan(h, n_local, m, a, b, c, d, const_cast<double*>(d), !last, 32, false))) return r;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  h->last_stream = st;
-  const bool zf = rank == 0, zl = last;
-  const size_t top = h->levels.size() - 1;
-  for (size_t k = 0; k < top; ++k)
-    if ((r = enq_reduce(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
-  double* out4[4] = {iface, iface + 2, iface + 4, iface + 6};
-  return enq_reduce(h, top, 0, 1, st, zf, zl, 0, out4);
+  return dist_reduce_impl<double>(h, a, b, c, d, n_local, m, rank, world, iface, stream);
+}
+int pm_dist_reduce_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                       const float* d, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                       float* iface, void* stream) {
+  return dist_reduce_impl<float>(h, a, b, c, d, n_local, m, rank, world, iface, stream);
 }
 
 int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const double* c,
                       const double* d, double* x, int64_t n_local, int32_t m, int32_t rank,
                       int32_t world, const double* iface_all, void* stream) {
-  int r = validate_common(h, a, b, c, d, x, n_local, m);
-  if (r) return r;
-  if (!iface_all) return fail(h, PM_ERR_VALIDATION, "null iface_all pointer");
-  if (world < 1 || rank < 0 || rank >= world)
-    return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
-  const bool last = rank == world - 1;
-  if (!last && n_local % m != 0)
-    return fail(h, PM_ERR_VALIDATION, "n_local must be a multiple of m on every rank but the last");
-  PM_CUDA(h, cudaSetDevice(h->device));
-  h->launches = 0;
-  // two extra doubles in front of the level scratch hold this rank's (xf, xl)
-  if ((r = build_plan(h, n_local, m, a, b, c, d, x, !last, 32, false))) return r;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  h->last_stream = st;
-  double* xb = h->scratch;  // extra_doubles region
-  PM_CUDA(h, pm::launch_dist_chain(iface_all, world, rank, xb, h->dflag, st));
-  ++h->launches;
-  const bool zf = rank == 0, zl = last;
-  const size_t top = h->levels.size() - 1;
-  if ((r = enq_solve(h, top, 0, 1, st, zf, zl, 0, xb))) return r;
-  for (size_t k = top; k-- > 0;)
-    if ((r = enq_solve(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
-  return PM_OK;
+  return dist_solve_impl<double>(h, a, b, c, d, x, n_local, m, rank, world, iface_all, stream);
+}
+int pm_dist_solve_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                      const float* d, float* x, int64_t n_local, int32_t m, int32_t rank,
+                      int32_t world, const float* iface_all, void* stream) {
+  return dist_solve_impl<float>(h, a, b, c, d, x, n_local, m, rank, world, iface_all, stream);
 }
 
 int pm_last_launch_count(pm_handle_t h) { return h ? h->launches : -1; }

@@ -70,12 +70,13 @@ class DistributedSolver:
 
         n = int(len(b))
         for t in (a, b, c, d, x):
-            if not (isinstance(t, np.ndarray) and t.dtype == np.float64 and t.flags.c_contiguous
-                    and len(t) == n):
-                raise ValidationError("host arrays must be contiguous float64 of equal length")
+            if not (isinstance(t, np.ndarray) and t.dtype == b.dtype and t.dtype in (np.float64, np.float32)
+                    and t.flags.c_contiguous and len(t) == n):
+                raise ValidationError("host arrays must be contiguous float64/float32 of equal length")
         dev = self.iface.device
-        if getattr(self, "_stage", None) is None or self._stage.shape[1] < n:
-            self._stage = torch.empty((5, n), dtype=torch.float64, device=dev)
+        tdt = torch.float64 if b.dtype == np.float64 else torch.float32
+        if getattr(self, "_stage", None) is None or self._stage.shape[1] < n or self._stage.dtype != tdt:
+            self._stage = torch.empty((5, n), dtype=tdt, device=dev)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         da, db, dc, dd, dx = (self._stage[k, :n] for k in range(5))
         with torch.cuda.stream(st):
@@ -89,6 +90,9 @@ class DistributedSolver:
         return x
 
     def solve(self, a, b, c, d, x, m: int = 10, stream=None):
+        if self.iface.dtype != b.dtype:  # FP32 solve: interface equations in FP32
+            self.iface = self.iface.to(b.dtype)
+            self.iface_all = self.iface_all.to(b.dtype)
         self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
         self._all_gather()
         self.solver.dist_solve(a, b, c, d, x, m, self.rank, self.world, self.iface_all, stream=stream)

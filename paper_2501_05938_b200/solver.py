@@ -51,17 +51,29 @@ class StageTimings:
     t3_d2h: float = 0.0
 
 
-def _check_host(*arrs):
+def _check_host(*arrs, dtype=np.float64):
     for x in arrs:
-        if not isinstance(x, np.ndarray) or x.dtype != np.float64 or not x.flags.c_contiguous:
-            raise ValidationError("host arrays must be C-contiguous float64 numpy arrays")
+        if not isinstance(x, np.ndarray) or x.dtype != dtype or not x.flags.c_contiguous:
+            raise ValidationError(f"host arrays must be C-contiguous {np.dtype(dtype).name} numpy arrays")
 
 
-def _dev_ptr(t, n: Optional[int] = None) -> int:
+def _suffix(dtype) -> str:
+    """C ABI precision suffix of a torch / numpy dtype: FP64 (the north_star
+    solver) or FP32 (the paper's FP32 experiments)."""
+    name = str(dtype).replace("torch.", "")
+    if name == "float64":
+        return "f64"
+    if name == "float32":
+        return "f32"
+    raise ValidationError("arrays must be float64 or float32")
+
+
+def _dev_ptr(t, n: Optional[int] = None, dtype=None) -> int:
     import torch
 
-    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
-        raise ValidationError("device arrays must be float64 CUDA tensors")
+    dtype = dtype if dtype is not None else torch.float64
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or not t.is_cuda:
+        raise ValidationError(f"device arrays must be {str(dtype).replace('torch.', '')} CUDA tensors")
     if not t.is_contiguous():
         raise ValidationError("device arrays must be contiguous")
     if n is not None and t.numel() < n:
@@ -141,66 +153,71 @@ class PartitionSolver:
 
     # -- solves -----------------------------------------------------------------
     def solve_host(self, a, b, c, d, m: int = 10, num_streams: int = 0, out=None) -> np.ndarray:
-        """pm_solve_host_f64: host arrays in, x out (copies overlap compute when
-        the arrays are page-locked, e.g. `pinned_empty`)."""
-        _check_host(a, b, c, d)
+        """pm_solve_host_f64 / _f32 (by the arrays' dtype): host arrays in, x out
+        (copies overlap compute when the arrays are page-locked, e.g.
+        `pinned_empty`)."""
+        dt = b.dtype if isinstance(b, np.ndarray) else np.float64
+        sfx = _suffix(dt)
+        _check_host(a, b, c, d, dtype=dt)
         n = b.shape[0]
         if not (a.shape[0] == c.shape[0] == d.shape[0] == n):
             raise ValidationError("a, b, c, d must have the same length")
-        x = out if out is not None else np.empty(n, np.float64)
-        _check_host(x)
-        self._ok(self._L.pm_solve_host_f64(self._h, a.ctypes.data, b.ctypes.data, c.ctypes.data,
-                                           d.ctypes.data, x.ctypes.data, n, m, num_streams))
+        x = out if out is not None else np.empty(n, dt)
+        _check_host(x, dtype=dt)
+        fn = getattr(self._L, "pm_solve_host_" + sfx)
+        self._ok(fn(self._h, a.ctypes.data, b.ctypes.data, c.ctypes.data, d.ctypes.data, x.ctypes.data, n,
+                    m, num_streams))
         return x
 
     def solve_device(self, a, b, c, d, m: int = 10, out=None, stream=None, n: Optional[int] = None):
-        """pm_solve_device_f64 (asynchronous; `check()` reports pivot failures)."""
+        """pm_solve_device_f64 / _f32 by b's dtype (asynchronous; `check()`
+        reports pivot failures)."""
         import torch
 
+        dt = b.dtype
+        fn = getattr(self._L, "pm_solve_device_" + _suffix(dt))
         n = int(b.numel()) if n is None else n
-        x = out if out is not None else torch.empty(n, dtype=torch.float64, device=b.device)
-        self._ok(self._L.pm_solve_device_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
-                                             _dev_ptr(d, n), _dev_ptr(x, n), n, m,
-                                             _stream_handle(stream)))
+        x = out if out is not None else torch.empty(n, dtype=dt, device=b.device)
+        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
+                    _dev_ptr(x, n, dt), n, m, _stream_handle(stream)))
         return x
 
     def solve_batch_device(self, a, b, c, d, n_per_system: int, m: int = 10, out=None, stream=None):
         import torch
 
+        dt = b.dtype
+        fn = getattr(self._L, "pm_solve_batch_device_" + _suffix(dt))
         n = int(b.numel())
         if n_per_system < 1 or n % n_per_system:
             raise ValidationError("array length must be a multiple of n_per_system")
-        x = out if out is not None else torch.empty(n, dtype=torch.float64, device=b.device)
-        self._ok(self._L.pm_solve_batch_device_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
-                                                   _dev_ptr(d, n), _dev_ptr(x, n), n_per_system,
-                                                   n // n_per_system, m, _stream_handle(stream)))
+        x = out if out is not None else torch.empty(n, dtype=dt, device=b.device)
+        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
+                    _dev_ptr(x, n, dt), n_per_system, n // n_per_system, m, _stream_handle(stream)))
         return x
 
     def check(self):
         """pm_check: synchronise and raise ComputationError on a pivot failure."""
         self._ok(self._L.pm_check(self._h))
 
-    def generate_device(self, n: int, seed: int = 42, device=None, stream=None, arrays=None):
-        """pm_generate_f64 into (new or given) CUDA tensors a, b, c, d."""
-        import torch
-
-        dev = device if device is not None else torch.device("cuda", self.device)
-        if arrays is None:
-            arrays = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(4)]
-        self._ok(self._L.pm_generate_f64(self._h, *[_dev_ptr(t, n) for t in arrays], n, seed,
-                                         _stream_handle(stream)))
-        return arrays
+    def generate_device(self, n: int, seed: int = 42, device=None, stream=None, arrays=None, dtype=None):
+        """pm_generate_f64 / _f32 into (new or given) CUDA tensors a, b, c, d."""
+        return self.generate_range_device(n, 0, n, seed, device=device, stream=stream, arrays=arrays,
+                                          dtype=dtype)
 
     def generate_range_device(self, n_total: int, row0: int, count: int, seed: int = 42, device=None,
-                              stream=None, arrays=None):
-        """pm_generate_range_f64: rows [row0, row0+count) of the n_total system."""
+                              stream=None, arrays=None, dtype=None):
+        """pm_generate_range_f64 / _f32: rows [row0, row0+count) of the n_total system."""
         import torch
 
         dev = device if device is not None else torch.device("cuda", self.device)
+        if arrays is not None:
+            dtype = arrays[1].dtype
+        dtype = dtype if dtype is not None else torch.float64
         if arrays is None:
-            arrays = [torch.empty(count, dtype=torch.float64, device=dev) for _ in range(4)]
-        self._ok(self._L.pm_generate_range_f64(self._h, *[_dev_ptr(t, count) for t in arrays], n_total,
-                                               row0, count, seed, _stream_handle(stream)))
+            arrays = [torch.empty(count, dtype=dtype, device=dev) for _ in range(4)]
+        fn = getattr(self._L, "pm_generate_range_" + _suffix(dtype))
+        self._ok(fn(self._h, *[_dev_ptr(t, count, dtype) for t in arrays], n_total, row0, count, seed,
+                    _stream_handle(stream)))
         return arrays
 
     def kernel_times(self, max_records: int = 65536):
@@ -223,16 +240,17 @@ class PartitionSolver:
 
     # -- row-sharded single system (BASELINE.json config 5) ---------------------
     def dist_reduce(self, a, b, c, d, m: int, rank: int, world: int, iface, stream=None):
-        n = int(b.numel())
-        self._ok(self._L.pm_dist_reduce_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
-                                            _dev_ptr(d, n), n, m, rank, world, _dev_ptr(iface, 8),
-                                            _stream_handle(stream)))
+        n, dt = int(b.numel()), b.dtype
+        fn = getattr(self._L, "pm_dist_reduce_" + _suffix(dt))
+        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt), n,
+                    m, rank, world, _dev_ptr(iface, 8, dt), _stream_handle(stream)))
 
     def dist_solve(self, a, b, c, d, x, m: int, rank: int, world: int, iface_all, stream=None):
-        n = int(b.numel())
-        self._ok(self._L.pm_dist_solve_f64(self._h, _dev_ptr(a, n), _dev_ptr(b, n), _dev_ptr(c, n),
-                                           _dev_ptr(d, n), _dev_ptr(x, n), n, m, rank, world,
-                                           _dev_ptr(iface_all, 8 * world), _stream_handle(stream)))
+        n, dt = int(b.numel()), b.dtype
+        fn = getattr(self._L, "pm_dist_solve_" + _suffix(dt))
+        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
+                    _dev_ptr(x, n, dt), n, m, rank, world, _dev_ptr(iface_all, 8 * world, dt),
+                    _stream_handle(stream)))
 
     # -- stream-count model -------------------------------------------------------
     def set_model_bundle(self, bundle: "ModelBundleC"):
@@ -244,11 +262,12 @@ class PartitionSolver:
         return b
 
 
-def pinned_empty(n: int) -> np.ndarray:
-    """A page-locked float64 host array (torch's pinned allocator)."""
+def pinned_empty(n: int, dtype=np.float64) -> np.ndarray:
+    """A page-locked host array (torch's pinned allocator), float64 or float32."""
     import torch
 
-    return torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+    return torch.empty(n, dtype=tdt, pin_memory=True).numpy()
 
 
 def recommend_streams(n: int, bundle=None) -> int:
