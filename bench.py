@@ -36,6 +36,8 @@ import tempfile
 import time
 from pathlib import Path
 
+import numpy as np
+
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -58,6 +60,8 @@ def parse():
     p.add_argument("--batch", type=int, default=4096)
     p.add_argument("--batch-rows", type=int, default=100_000)
     p.add_argument("--rows-per-gpu", type=float, default=8e7, help="rows per GPU (N)")
+    p.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                   help="f32: the FP32 solver (pm_*_f32, PAPER.md:243-274); bytes per unknown halve")
     p.add_argument("--m", type=int, default=10)
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--e2e-steps", type=int, default=5)
@@ -343,6 +347,9 @@ def main():
     if args.workload == "batch":
         return run_batch(args, world, rank, local)
     m = args.m
+    rdt = torch.float64 if args.precision == "f64" else torch.float32
+    esz = 8 if args.precision == "f64" else 4  # bytes per real
+    b_solve, b_reduce, b_total = BYTES_SOLVE * esz / 8, BYTES_REDUCE * esz / 8, BYTES_TOTAL * esz / 8
     n_rank = int(args.rows_per_gpu)
     n_total = n_rank * world
     rows = split_rows(n_total, world, m)
@@ -357,8 +364,8 @@ def main():
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     with torch.cuda.stream(stream):
-        a, b, c, d = solver.generate_range_device(n_total, row0, n_loc, args.seed, stream=sh)
-        x = torch.empty(n_loc, dtype=torch.float64, device="cuda")
+        a, b, c, d = solver.generate_range_device(n_total, row0, n_loc, args.seed, stream=sh, dtype=rdt)
+        x = torch.empty(n_loc, dtype=rdt, device="cuda")
     torch.cuda.synchronize()
     dsolver = DistributedSolver(solver) if world > 1 else None
 
@@ -444,8 +451,8 @@ def main():
     per_kernel = {k: round(sum(v) / len(v), 5) for k, v in sorted(per_kernel.items())}
     t_kern_total = sum(t for (_, _, t) in ktimes) / args.steps
     peak, peak_src = peaks()
-    ach_solve = BYTES_SOLVE * n_loc / (t_solve / 1e3) / 1e9
-    ach_reduce = BYTES_REDUCE * n_loc / (t_reduce / 1e3) / 1e9
+    ach_solve = b_solve * n_loc / (t_solve / 1e3) / 1e9
+    ach_reduce = b_reduce * n_loc / (t_reduce / 1e3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
@@ -461,7 +468,7 @@ def main():
     # rows, row-sharded solve with the NCCL all-gather, D2H), max over ranks.
     e2e = None
     if not args.no_e2e:
-        host = [pinned_empty(n_loc) for _ in range(5)]
+        host = [pinned_empty(n_loc, np.float64 if esz == 8 else np.float32) for _ in range(5)]
         for hbuf, t in zip(host, (a, b, c, d)):
             torch.from_numpy(hbuf).copy_(t)  # the same synthetic rows, staged once
         del a, b, c, d
@@ -491,11 +498,11 @@ def main():
             t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             t_e2e = float(t.item())
-        e2e = {"value": n_total / t_e2e, "unit": "unknowns/s", "h2d_bytes_per_step": 32 * n_total,
-               "d2h_bytes_per_step": 8 * n_total, "ms_per_step": t_e2e * 1e3,
+        e2e = {"value": n_total / t_e2e, "unit": "unknowns/s", "h2d_bytes_per_step": 4 * esz * n_total,
+               "d2h_bytes_per_step": esz * n_total, "ms_per_step": t_e2e * 1e3,
                "num_streams": used if world == 1 else None,
-               "link_gbs_per_gpu": 40 * n_loc / t_e2e / 1e9, "steps": args.e2e_steps,
-               "timing": ("host wall clock around pm_solve_host_f64, median" if world == 1 else
+               "link_gbs_per_gpu": 5 * esz * n_loc / t_e2e / 1e9, "steps": args.e2e_steps,
+               "timing": ("host wall clock around pm_solve_host_%s, median" % args.precision if world == 1 else
                           "host wall clock around DistributedSolver.solve_host per rank, median, max over ranks")}
         if args.check:
             ce = gather_check(torch.from_numpy(xs))
@@ -503,7 +510,7 @@ def main():
                 check["e2e"] = ce
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.precision == "f64":
         cores, model = cpu_info()
         ups, threads, times = cpu_partition_baseline(n_loc, m, args.seed, reps=3)
         cpu = {"value": ups, "unit": "unknowns/s", "cores": threads, "kind": "port",
@@ -515,22 +522,23 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (counter-based generator, seed %d)" % args.seed,
-            "config": {"workload": "device-resident single SLAE, N=8e7 rows per GPU, FP64, m=%d "
-                                   "(BASELINE config 3; N>1: one system row-sharded, config 5)" % m,
+            "config": {"workload": "device-resident single SLAE, N=8e7 rows per GPU, %s, m=%d "
+                                   "(BASELINE config 3; N>1: one system row-sharded, config 5)"
+                                   % ("FP64" if esz == 8 else "FP32 (PAPER.md:243-274 variant)", m),
                        "n_total": n_total, "n_per_gpu": n_rank, "m": m,
                        "parallelism": "row-sharded x%d" % world if world > 1 else "single GPU",
-                       "l2": "inputs 2.56 GB/GPU > 126 MB L2 (no flush needed)"},
+                       "l2": "inputs %.2f GB/GPU > 126 MB L2 (no flush needed)" % (4 * esz * n_loc / 1e9)},
             "roofline": {"bound": "hbm", "achieved": ach_solve, "peak": peak, "unit": "GB/s",
-                         "frac": ach_solve / peak, "traffic": traffic,
-                         "kernel": "Stage 3 (SOLVE level 0): 40 B/unknown", "peak_source": peak_src,
+                         "frac": ach_solve / peak, "traffic": traffic if esz == 8 else None,
+                         "kernel": "Stage 3 (SOLVE level 0): %g B/unknown" % b_solve, "peak_source": peak_src,
                          "kernel_ms": t_solve,
                          "stage1": {"achieved": ach_reduce, "frac": ach_reduce / peak,
-                                    "kernel_ms": t_reduce, "bytes_per_unknown": BYTES_REDUCE},
-                         "whole_solve": {"achieved": BYTES_TOTAL * n_loc / (ms_per_step / 1e3) / 1e9,
-                                         "frac": BYTES_TOTAL * n_loc / (ms_per_step / 1e3) / 1e9 / peak,
-                                         "bytes_per_unknown": BYTES_TOTAL,
+                                    "kernel_ms": t_reduce, "bytes_per_unknown": b_reduce},
+                         "whole_solve": {"achieved": b_total * n_loc / (ms_per_step / 1e3) / 1e9,
+                                         "frac": b_total * n_loc / (ms_per_step / 1e3) / 1e9 / peak,
+                                         "bytes_per_unknown": b_total,
                                          "kernel_ms_sum": t_kern_total},
                          "kernels_ms": per_kernel},
             "e2e": e2e,

@@ -43,17 +43,20 @@ SIZES = [int(k * 10**i) for i in range(3, 8) for k in (1, 2.5, 4, 5, 7.5, 8)]
 COUNTS = [1, 2, 4, 8, 16, 32]
 
 
-def synthetic(n: int, seed: int = 42):
+def synthetic(n: int, seed: int = 42, precision: str = "f64"):
     """The counter-based system, generated on the device and copied to pinned
-    host buffers (the same bits as the CPU oracle's generator)."""
+    host buffers (the same bits as the CPU oracle's generator; FP32: their
+    round-to-nearest images)."""
+    import numpy as np
     import torch
 
+    dt = torch.float64 if precision == "f64" else torch.float32
     s = PartitionSolver(0)
-    arrs = s.generate_device(n, seed)
+    arrs = s.generate_device(n, seed, dtype=dt)
     torch.cuda.synchronize()
     host = []
     for t in arrs:
-        h = pinned_empty(n)
+        h = pinned_empty(n, np.float64 if precision == "f64" else np.float32)
         h[:] = t.cpu().numpy()
         host.append(h)
     s.close()
@@ -61,13 +64,13 @@ def synthetic(n: int, seed: int = 42):
     return host
 
 
-def sweep(sizes, reps: int, stream_mode: int, m: int = 10):
+def sweep(sizes, reps: int, stream_mode: int, m: int = 10, precision: str = "f64"):
     solver = PartitionSolver(0)
     solver.set_option(PM_OPT_STREAM_MODE, stream_mode)
     stage_rows, run_rows, raw = [], [], {}
     for n in sizes:
-        a, b, c, d = synthetic(n)
-        x = pinned_empty(n)
+        a, b, c, d = synthetic(n, precision=precision)
+        x = pinned_empty(n, b.dtype)
         # warm-up every count once (stream pools, allocations)
         for ns in COUNTS:
             solver.solve_host(a, b, c, d, m=m, num_streams=ns, out=x)
@@ -125,6 +128,27 @@ def validate(bundle, run_rows):
     return out
 
 
+def validate_fp32(bundle64, bundle32, run_rows):
+    """Table 5 on B200: the measured FP32 optimum against the paper's halving
+    rule applied to the FP64 bundle (recommend_fp32) and against
+    the FP32 re-fit's own recommendation."""
+    by = {}
+    for n, ns, t in run_rows:
+        by.setdefault(n, {})[ns] = t
+    out = []
+    for n in sorted(by):
+        meas = min(by[n], key=lambda k: by[n][k])
+        half = st.recommend_fp32(bundle64, n)
+        fit = st.recommend(bundle32, n).chosen
+        out.append({"slae_size": n, "measured_opt_fp32": meas, "fp64_choice": st.recommend(bundle64, n).chosen,
+                    "halving_rule": half, "fp32_fit": fit,
+                    "halving_within_one_power_of_two": max(half, meas) / min(half, meas) <= 2,
+                    "fit_within_one_power_of_two": max(fit, meas) / min(fit, meas) <= 2,
+                    "t_half_over_t_best": by[n][half] / by[n][meas],
+                    "t_fit_over_t_best": by[n][fit] / by[n][meas]})
+    return out
+
+
 def write_inc(bundle, path: Path, note: str):
     path.write_text(
         "// Generated by tools/refit.py -- the B200 re-fit of the paper's Eq. 4 / Eq. 7\n"
@@ -143,18 +167,20 @@ def main():
     p.add_argument("--max-size", type=float, default=8e7)
     p.add_argument("--threshold", type=int, default=1_000_000)
     p.add_argument("--install", action="store_true")
+    p.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                   help="f32: the FP32 sweep (pm_solve_host_f32) and Table 5 on B200")
     args = p.parse_args()
     out = ROOT / args.out
     out.mkdir(parents=True, exist_ok=True)
     sizes = [n for n in SIZES if n <= args.max_size]
     t0 = time.time()
-    stage_rows, run_rows, raw = sweep(sizes, args.reps, args.stream_mode)
+    stage_rows, run_rows, raw = sweep(sizes, args.reps, args.stream_mode, precision=args.precision)
     stage_csv, runs_csv = to_csv(stage_rows, run_rows)
     (out / "stage_timings.csv").write_text(stage_csv)
     (out / "streamed_runs.csv").write_text(runs_csv)
     (out / "raw_times.json").write_text(json.dumps(raw))
     bundle, met = st.fit_bundle(stage_csv, runs_csv, size_threshold=args.threshold, seed=42)
-    bundle.provenance.update({"fitted_on": "NVIDIA B200 (tools/refit.py, pm_solve_host_f64, m=10)",
+    bundle.provenance.update({"fitted_on": f"NVIDIA B200 (tools/refit.py, pm_solve_host_{args.precision}, m=10)",
                               "stream_mode": "pooled" if args.stream_mode == 0 else "created per solve",
                               "reps": args.reps, "sweep_seconds": round(time.time() - t0, 1)})
     (out / "bundle.json").write_text(json.dumps(bundle.to_document(), indent=1))
@@ -164,9 +190,19 @@ def main():
     summary = {"sizes": len(val), "exact": exact, "within_one_power_of_two": ok,
                "worst_t_pred_over_t_best": max(v["t_pred_over_t_best"] for v in val),
                "metrics": met, "rows": val}
+    if args.precision == "f32":
+        t5 = validate_fp32(st.ModelBundle.b200(), bundle, run_rows)
+        summary["table5_b200"] = {
+            "halving_exact": sum(r["halving_rule"] == r["measured_opt_fp32"] for r in t5),
+            "halving_within_one_power_of_two": sum(r["halving_within_one_power_of_two"] for r in t5),
+            "fp32_fit_exact": sum(r["fp32_fit"] == r["measured_opt_fp32"] for r in t5),
+            "fp32_fit_within_one_power_of_two": sum(r["fit_within_one_power_of_two"] for r in t5),
+            "worst_t_half_over_t_best": max(r["t_half_over_t_best"] for r in t5),
+            "rows": t5}
     (out / "validation.json").write_text(json.dumps(summary, indent=1))
-    print(json.dumps({k: v for k, v in summary.items() if k != "rows"}, indent=1))
-    if args.install:
+    print(json.dumps({k: (v if k != "table5_b200" else {kk: vv for kk, vv in v.items() if kk != "rows"})
+                      for k, v in summary.items() if k != "rows"}, indent=1))
+    if args.install and args.precision == "f64":
         write_inc(bundle, ROOT / "paper_2501_05938_b200" / "csrc" / "streamtune" / "b200_bundle.inc",
                   f"{len(val)} sizes x {len(COUNTS)} stream counts, {args.reps} reps, "
                   f"{'pooled' if args.stream_mode == 0 else 'per-solve'} streams")
