@@ -250,8 +250,7 @@ __global__ void __launch_bounds__(512, 1) batch_cluster_kernel(BatchArgs args) {
       double xv[M];
       block_solve_pairs<M>(pa, xf, xl, xv, bad);
       __syncwarp();
-#pragma unroll
-      for (int j = 0; j < M; ++j) bad |= !isfinite(xv[j]);
+      bad |= !all_finite<M>(xv);
       if constexpr ((M % 2) == 0) {
 #pragma unroll
         for (int j = 0; j < M / 2; ++j)

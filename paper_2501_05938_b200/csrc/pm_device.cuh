@@ -102,6 +102,65 @@ __device__ __forceinline__ float pow2_inv_scale(float u, float v) {
   return __int_as_float((127 - e) << 23);
 }
 
+// Pivot reciprocals of a block from its continuants: inv[j] = q[j-1] / q[j],
+// j = 1..L.  PM_BATCH_INV (default): one reciprocal for all L pivots
+// (Montgomery's batch inversion: P_j = q_1 ... q_j, R = 1/P_L, then
+// 1/q_j = R * P_{j-1} and R <- R * q_j walking down) -- 2 multiplies per
+// pivot instead of a MUFU + Newton sequence each.  Returns false when the
+// product leaves the safe range (the caller then takes the classic sweep).
+#ifndef PM_BATCH_INV
+#define PM_BATCH_INV 1
+#endif
+#ifdef PM_REAL_F32
+constexpr real kProdLo = 1e-30f, kProdHi = 1e30f;
+#else
+constexpr real kProdLo = 1e-250, kProdHi = 1e250;
+#endif
+template <int L>
+__device__ __forceinline__ bool continuant_ratios(const real (&q)[L + 1], real (&inv)[L + 1]) {
+#if PM_BATCH_INV
+  real P[L + 1];
+  P[1] = q[1];
+#pragma unroll
+  for (int j = 2; j <= L; ++j) P[j] = P[j - 1] * q[j];
+  const real aP = fabs(P[L]);
+  if (!(aP > kProdLo && aP < kProdHi)) return false;
+  real R = drcp(P[L]);
+#pragma unroll
+  for (int j = L; j >= 2; --j) {
+    const real iq = R * P[j - 1];  // 1 / q_j
+    R = R * q[j];                  // 1 / P_{j-1}
+    inv[j] = q[j - 1] * iq;
+  }
+  inv[1] = R;  // q_0 = 1
+  return true;
+#else
+#pragma unroll
+  for (int j = 1; j <= L; ++j) inv[j] = q[j - 1] * drcp(q[j]);
+  return true;
+#endif
+}
+
+// Finiteness of a block's results with one compare: fma(x, 0, t) keeps t = 0
+// for finite x and turns it into NaN for an inf / NaN x.
+#ifndef PM_FINITE_SUM
+#define PM_FINITE_SUM 1
+#endif
+template <int M>
+__device__ __forceinline__ bool all_finite(const real (&x)[M]) {
+#if PM_FINITE_SUM
+  real t = 0.0;
+#pragma unroll
+  for (int j = 0; j < M; ++j) t = fma(x[j], real(0.0), t);
+  return t == real(0.0);
+#else
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < M; ++j) ok &= isfinite(x[j]);
+  return ok;
+#endif
+}
+
 // Merge segment A = [f1..l1] with its right neighbour B = [f2..l2], f2 = l1+1,
 // eliminating x[l1] and x[f2].  Division-free: both output equations are
 // multiplied by s*det (equations may be scaled freely), with s an exact
@@ -238,10 +297,8 @@ __device__ __forceinline__ Seg block_reduce_fast(Acc& r, bool& bad) {
       ok &= (q[j] != 0.0);
     }
     ok &= isfinite(q[L]) && (fabs(q[L]) > kTinyPivot);
-    if (ok) {
-#pragma unroll
-      for (int j = 1; j <= L; ++j) inv[j] = q[j - 1] * drcp(q[j]);
-    } else {  // classic sweep (rare)
+    if (ok) ok = continuant_ratios<L>(q, inv);
+    if (!ok) {  // classic sweep (rare)
       real cprev = 0.0;
 #pragma unroll
       for (int j = 1; j <= L; ++j) {

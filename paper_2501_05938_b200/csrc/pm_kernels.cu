@@ -606,8 +606,7 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
         real xv[(M > 0 ? M : 1)];
         block_solve_pairs<(M > 0 ? M : 1)>(pa, xf, xl, xv, bad);
         __syncwarp();
-#pragma unroll
-        for (int j = 0; j < M; ++j) bad |= !isfinite(xv[j]);
+        bad |= !all_finite<M>(xv);
         if constexpr ((M % 2) == 0) {
 #pragma unroll
           for (int j = 0; j < M / 2; ++j)

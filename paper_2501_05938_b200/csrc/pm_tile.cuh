@@ -336,10 +336,8 @@ __device__ __forceinline__ void block_solve_pairs(const PairAcc<M>& r, real xs, 
       ok &= (q[j] != 0.0);
     }
     ok &= isfinite(q[L]) && (fabs(q[L]) > kTinyPivot);
-    if (ok) {
-#pragma unroll
-      for (int j = 1; j <= L; ++j) inv[j] = q[j - 1] * drcp(q[j]);
-    } else {
+    if (ok) ok = continuant_ratios<L>(q, inv);
+    if (!ok) {
       real cprev = 0.0;
 #pragma unroll
       for (int j = 1; j <= L; ++j) {
