@@ -89,7 +89,7 @@ typedef struct pm_model_bundle {
                                   32*m rows; 0: CTA tiles (P*m rows, P <= 128)     */
 #define PM_OPT_SOLVE_STAGES 8  /* ring depth of the level-0 Stage-3 kernel
                                   (default 1; 0 = PM_OPT_STAGES)                   */
-#define PM_OPT_WARPS_PER_CTA 9 /* warps per CTA of the warp-tile kernels (1..8)    */
+#define PM_OPT_WARPS_PER_CTA 9 /* warps per CTA of the warp-tile kernels (1..4)    */
 #define PM_OPT_CHAIN 10        /* 1: level-0 warps chain contiguous tile chunks, so
                                   level 1 is a single ROOT tile (default 0)        */
 #define PM_OPT_UPPER_M 11      /* rows per thread of the warp-tile upper levels

@@ -897,7 +897,7 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       h->root_m = (int)value;
       return PM_OK;
     case PM_OPT_WARPS_PER_CTA:
-      if (value < 1 || value > 8) return fail(h, PM_ERR_VALIDATION, "warps per CTA must lie in [1, 8]");
+      if (value < 1 || value > 4) return fail(h, PM_ERR_VALIDATION, "warps per CTA must lie in [1, 4]");
       h->warps_per_cta = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_CLUSTER:
