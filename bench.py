@@ -69,6 +69,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--num-streams", type=int, default=0, help="e2e stream count (0 = predictor)")
     p.add_argument("--dist-backend", default="nccl", help="torch.distributed backend (tests: gloo)")
+    p.add_argument("--exchange", default="auto", choices=["auto", "p2p", "collective"],
+                   help="N>1 interface exchange: peer memory (CUDA IPC over NVLink, in-kernel flags) "
+                        "or an all-gather; auto = p2p when the mapping self-test passes")
     p.add_argument("--same-device", action="store_true",
                    help="tests only: every rank on cuda:0 (with --dist-backend gloo)")
     p.add_argument("--check", action="store_true",
@@ -367,7 +370,7 @@ def main():
         a, b, c, d = solver.generate_range_device(n_total, row0, n_loc, args.seed, stream=sh, dtype=rdt)
         x = torch.empty(n_loc, dtype=rdt, device="cuda")
     torch.cuda.synchronize()
-    dsolver = DistributedSolver(solver) if world > 1 else None
+    dsolver = DistributedSolver(solver, exchange=args.exchange) if world > 1 else None
 
     def step():
         if dsolver is None:
@@ -529,6 +532,7 @@ def main():
                                    % ("FP64" if esz == 8 else "FP32 (PAPER.md:243-274 variant)", m),
                        "n_total": n_total, "n_per_gpu": n_rank, "m": m,
                        "parallelism": "row-sharded x%d" % world if world > 1 else "single GPU",
+                       "exchange": (dsolver.exchange if dsolver is not None else None),
                        "l2": "inputs %.2f GB/GPU > 126 MB L2 (no flush needed)" % (4 * esz * n_loc / 1e9)},
             "roofline": {"bound": "hbm", "achieved": ach_solve, "peak": peak, "unit": "GB/s",
                          "frac": ach_solve / peak, "traffic": traffic if esz == 8 else None,
@@ -550,6 +554,7 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        dsolver.close()
         dist.destroy_process_group()
     solver.close()
     return 0

@@ -190,6 +190,37 @@ int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const dou
                       const double* d, double* x, int64_t n_local, int32_t m, int32_t rank,
                       int32_t world, const double* iface_all, void* stream);
 
+/* Peer-memory (NVLink P2P) exchange of the interface equations -- the
+ * all-gather of pm_dist_* done by the solver's own kernels.  Each rank
+ * allocates an exchange buffer (pm_dist_exchange_alloc; owned by the handle),
+ * exports it with pm_ipc_get_handle, receives the peers' handles by any
+ * side channel (e.g. torch.distributed), maps them with pm_ipc_open_handle
+ * and calls pm_dist_set_peers with every rank's buffer in rank order (its
+ * own included).  Then per solve, on every rank:
+ *   pm_dist_reduce_p2p_*  Stage 1 + local levels, then one kernel stores the
+ *                         rank's 8 interface reals into every peer's buffer
+ *                         and releases an epoch flag (system scope);
+ *   pm_dist_solve_p2p_*   one thread acquires all ranks' flags, solves the
+ *                         2*world-row interface system, then Stage 3.
+ * No host synchronisation or collective call on the data path.  A peer that
+ * never publishes makes the wait time out after 20 s (PM_ERR_RUNTIME from
+ * pm_check).  Ranks must call the pair in lockstep (collective semantics). */
+#define PM_IPC_HANDLE_BYTES 64
+int64_t pm_dist_exchange_bytes(int32_t world);
+int pm_dist_exchange_alloc(pm_handle_t h, int32_t world, void** out);
+int pm_dist_set_peers(pm_handle_t h, void* const* peer_bufs, int32_t world, int32_t rank);
+int pm_ipc_get_handle(const void* dptr, void* handle_out);
+int pm_ipc_open_handle(const void* handle, void** dptr_out);
+int pm_ipc_close_handle(void* dptr);
+int pm_dist_reduce_p2p_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                           const double* d, int64_t n_local, int32_t m, void* stream);
+int pm_dist_solve_p2p_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                          const double* d, double* x, int64_t n_local, int32_t m, void* stream);
+int pm_dist_reduce_p2p_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                           const float* d, int64_t n_local, int32_t m, void* stream);
+int pm_dist_solve_p2p_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                          const float* d, float* x, int64_t n_local, int32_t m, void* stream);
+
 /* FP32 variants (the paper's FP32 experiments; Table 5 and
  * streamtune::recommend_fp32): the same pipeline, plan, options and status
  * codes on float arrays -- half the HBM and host-link bytes per unknown.

@@ -70,6 +70,17 @@ PM_SIGNATURES = [
      [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),
     ("pm_dist_solve_f32", C.c_int,
      [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),
+    # P2P interface exchange
+    ("pm_dist_exchange_bytes", C.c_int64, [C.c_int32]),
+    ("pm_dist_exchange_alloc", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("pm_dist_set_peers", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_int32]),
+    ("pm_ipc_get_handle", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("pm_ipc_open_handle", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("pm_ipc_close_handle", C.c_int, [C.c_void_p]),
+    ("pm_dist_reduce_p2p_f64", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
+    ("pm_dist_solve_p2p_f64", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
+    ("pm_dist_reduce_p2p_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
+    ("pm_dist_solve_p2p_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
     ("pm_last_launch_count", C.c_int, [C.c_void_p]),
     ("pm_kernel_times", C.c_int,
      [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int32]),

@@ -79,8 +79,13 @@ struct Prec<double> {
   }
   static size_t tile_smem(int mode, int P, int m, int S) { return pm::tile_smem_bytes(mode, P, m, S); }
   static size_t warp_smem(int mode, int m, int S) { return pm::warp_smem_bytes(mode, m, S); }
-  static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st) {
-    return pm::launch_dist_chain(ia, w, r, xb, f, st);
+  static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st,
+                                const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
+    return pm::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
+  }
+  static cudaError_t publish(const double* iface, void* const* peers, int w, int r, uint64_t e,
+                             cudaStream_t st) {
+    return pm::launch_dist_publish(iface, peers, w, r, e, st);
   }
   static cudaError_t generate(double* a, double* b, double* c, double* d, int64_t n, int64_t r0,
                               int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
@@ -102,8 +107,13 @@ struct Prec<float> {
   }
   static size_t tile_smem(int mode, int P, int m, int S) { return pm32::tile_smem_bytes(mode, P, m, S); }
   static size_t warp_smem(int mode, int m, int S) { return pm32::warp_smem_bytes(mode, m, S); }
-  static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st) {
-    return pm32::launch_dist_chain(ia, w, r, xb, f, st);
+  static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st,
+                                const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
+    return pm32::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
+  }
+  static cudaError_t publish(const float* iface, void* const* peers, int w, int r, uint64_t e,
+                             cudaStream_t st) {
+    return pm32::launch_dist_publish(iface, peers, w, r, e, st);
   }
   static cudaError_t generate(float* a, float* b, float* c, float* d, int64_t n, int64_t r0,
                               int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
@@ -157,6 +167,14 @@ struct pm_handle_s {
   int root_m = 8;    // ROOT tile: 128 * root_m rows
   std::vector<int64_t> part_chunks, part_base;
   void* chain_nodes = nullptr;
+  // P2P interface exchange (pm_dist_*_p2p): this rank's exchange buffer,
+  // the peers' buffers (device array), the rank's interface equations
+  char* xbuf = nullptr;
+  int xbuf_world = 0;
+  void** d_peers = nullptr;
+  int xworld = 0, xrank = -1;
+  uint64_t epoch = 0;
+  void* iface_local = nullptr;
   // per-launch CUDA-event timing (PM_OPT_KERNEL_TIMES)
   int ktimes = 0;
   std::vector<cudaEvent_t> kev;
@@ -504,6 +522,7 @@ int read_flag(pm_handle_t h, cudaStream_t st) {
   if (flag) {
     PM_CUDA(h, cudaMemsetAsync(h->dflag, 0, sizeof(int), st));
     PM_CUDA(h, cudaStreamSynchronize(st));
+    if (flag & 4) return fail(h, PM_ERR_RUNTIME, "P2P interface exchange timed out (a peer never published)");
     return fail(h, PM_ERR_COMPUTATION, "zero or non-finite pivot (system not solvable without pivoting)");
   }
   return PM_OK;
@@ -788,7 +807,8 @@ int dist_reduce_impl(pm_handle_t h, const R* a, const R* b, const R* c,
 template <class R>
 int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
                       const R* d, R* x, int64_t n_local, int32_t m, int32_t rank,
-                      int32_t world, const R* iface_all, void* stream) {
+                      int32_t world, const R* iface_all, void* stream,
+                      const uint64_t* flags = nullptr, uint64_t epoch = 0) {
   int r = validate_common(h, a, b, c, d, x, n_local, m);
   if (r) return r;
   if (!iface_all) return fail(h, PM_ERR_VALIDATION, "null iface_all pointer");
@@ -804,7 +824,8 @@ int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
   R* xb = reinterpret_cast<R*>(h->scratch);  // extra_elems region
-  PM_CUDA(h, Prec<R>::dist_chain(iface_all, world, rank, xb, h->dflag, st));
+  PM_CUDA(h, Prec<R>::dist_chain(iface_all, world, rank, xb, h->dflag, st, flags, epoch,
+                                  20ull * 1000 * 1000 * 1000 /* 20 s */));
   ++h->launches;
   const bool zf = rank == 0, zl = last;
   const size_t top = h->levels.size() - 1;
@@ -812,6 +833,42 @@ int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   for (size_t k = top; k-- > 0;)
     if ((r = enq_solve<R>(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
   return PM_OK;
+}
+
+// ---- P2P interface exchange (NVLink peer memory instead of the all-gather) --
+
+size_t exchange_bytes(int world) {
+  // [2][world][8] reals (sized for FP64; FP32 uses the first half) | [2][world] uint64
+  return (size_t)2 * world * 8 * sizeof(double) + (size_t)2 * world * sizeof(uint64_t);
+}
+
+template <class R>
+int dist_reduce_p2p_impl(pm_handle_t h, const R* a, const R* b, const R* c, const R* d,
+                         int64_t n_local, int32_t m, void* stream) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (!h->d_peers || h->xworld < 1) return fail(h, PM_ERR_VALIDATION, "pm_dist_set_peers not called");
+  if (!h->iface_local) PM_CUDA(h, cudaMalloc(&h->iface_local, 8 * sizeof(double)));
+  int r = dist_reduce_impl<R>(h, a, b, c, d, n_local, m, h->xrank, h->xworld,
+                              static_cast<R*>(h->iface_local), stream);
+  if (r) return r;
+  ++h->epoch;
+  PM_CUDA(h, Prec<R>::publish(static_cast<const R*>(h->iface_local), h->d_peers, h->xworld, h->xrank,
+                              h->epoch, static_cast<cudaStream_t>(stream)));
+  ++h->launches;
+  return PM_OK;
+}
+
+template <class R>
+int dist_solve_p2p_impl(pm_handle_t h, const R* a, const R* b, const R* c, const R* d, R* x,
+                        int64_t n_local, int32_t m, void* stream) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (!h->d_peers || !h->xbuf || h->xworld < 1)
+    return fail(h, PM_ERR_VALIDATION, "pm_dist_exchange_alloc / pm_dist_set_peers not called");
+  if (h->epoch == 0) return fail(h, PM_ERR_VALIDATION, "pm_dist_reduce_p2p must precede the solve");
+  const R* slots = reinterpret_cast<const R*>(h->xbuf);
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(slots + (size_t)2 * h->xworld * 8);
+  return dist_solve_impl<R>(h, a, b, c, d, x, n_local, m, h->xrank, h->xworld, slots, stream, flags,
+                            h->epoch);
 }
 
 extern "C" {
@@ -846,6 +903,9 @@ int pm_destroy(pm_handle_t h) {
   if (h->scratch) cudaFree(h->scratch);
   if (h->hbuf) cudaFree(h->hbuf);
   if (h->dflag) cudaFree(h->dflag);
+  if (h->xbuf) cudaFree(h->xbuf);
+  if (h->d_peers) cudaFree(h->d_peers);
+  if (h->iface_local) cudaFree(h->iface_local);
   delete h;
   return PM_OK;
 }
@@ -1074,6 +1134,83 @@ int pm_dist_solve_f32(pm_handle_t h, const float* a, const float* b, const float
                       const float* d, float* x, int64_t n_local, int32_t m, int32_t rank,
                       int32_t world, const float* iface_all, void* stream) {
   return dist_solve_impl<float>(h, a, b, c, d, x, n_local, m, rank, world, iface_all, stream);
+}
+
+int64_t pm_dist_exchange_bytes(int32_t world) {
+  return world < 1 ? -1 : (int64_t)exchange_bytes(world);
+}
+
+int pm_dist_exchange_alloc(pm_handle_t h, int32_t world, void** out) {
+  if (!h || !out || world < 1) return h ? fail(h, PM_ERR_VALIDATION, "world must be >= 1") : PM_ERR_VALIDATION;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  if (h->xbuf) {
+    PM_CUDA(h, cudaDeviceSynchronize());
+    PM_CUDA(h, cudaFree(h->xbuf));
+    h->xbuf = nullptr;
+  }
+  PM_CUDA(h, cudaMalloc(&h->xbuf, exchange_bytes(world)));
+  PM_CUDA(h, cudaMemset(h->xbuf, 0, exchange_bytes(world)));
+  h->xbuf_world = world;
+  h->epoch = 0;
+  *out = h->xbuf;
+  return PM_OK;
+}
+
+int pm_dist_set_peers(pm_handle_t h, void* const* peer_bufs, int32_t world, int32_t rank) {
+  if (!h || !peer_bufs) return PM_ERR_VALIDATION;
+  if (world < 1 || rank < 0 || rank >= world) return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  if (!h->xbuf || h->xbuf_world != world)
+    return fail(h, PM_ERR_VALIDATION, "pm_dist_exchange_alloc(world) must precede pm_dist_set_peers");
+  for (int k = 0; k < world; ++k)
+    if (!peer_bufs[k]) return fail(h, PM_ERR_VALIDATION, "null peer buffer");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  if (h->d_peers) PM_CUDA(h, cudaFree(h->d_peers));
+  PM_CUDA(h, cudaMalloc(&h->d_peers, sizeof(void*) * world));
+  PM_CUDA(h, cudaMemcpy(h->d_peers, peer_bufs, sizeof(void*) * world, cudaMemcpyHostToDevice));
+  h->xworld = world;
+  h->xrank = rank;
+  h->epoch = 0;
+  return PM_OK;
+}
+
+int pm_ipc_get_handle(const void* dptr, void* handle_out) {
+  if (!dptr || !handle_out) return PM_ERR_VALIDATION;
+  cudaIpcMemHandle_t hd;
+  if (cudaIpcGetMemHandle(&hd, const_cast<void*>(dptr)) != cudaSuccess) return PM_ERR_RUNTIME;
+  static_assert(sizeof(hd) == PM_IPC_HANDLE_BYTES, "CUDA IPC handle size");
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  return PM_OK;
+}
+
+int pm_ipc_open_handle(const void* handle, void** dptr_out) {
+  if (!handle || !dptr_out) return PM_ERR_VALIDATION;
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  if (cudaIpcOpenMemHandle(dptr_out, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return PM_ERR_RUNTIME;
+  return PM_OK;
+}
+
+int pm_ipc_close_handle(void* dptr) {
+  if (!dptr) return PM_ERR_VALIDATION;
+  return cudaIpcCloseMemHandle(dptr) == cudaSuccess ? PM_OK : PM_ERR_RUNTIME;
+}
+
+int pm_dist_reduce_p2p_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                           const double* d, int64_t n_local, int32_t m, void* stream) {
+  return dist_reduce_p2p_impl<double>(h, a, b, c, d, n_local, m, stream);
+}
+int pm_dist_reduce_p2p_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                           const float* d, int64_t n_local, int32_t m, void* stream) {
+  return dist_reduce_p2p_impl<float>(h, a, b, c, d, n_local, m, stream);
+}
+int pm_dist_solve_p2p_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                          const double* d, double* x, int64_t n_local, int32_t m, void* stream) {
+  return dist_solve_p2p_impl<double>(h, a, b, c, d, x, n_local, m, stream);
+}
+int pm_dist_solve_p2p_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                          const float* d, float* x, int64_t n_local, int32_t m, void* stream) {
+  return dist_solve_p2p_impl<float>(h, a, b, c, d, x, n_local, m, stream);
 }
 
 int pm_last_launch_count(pm_handle_t h) { return h ? h->launches : -1; }

@@ -740,11 +740,69 @@ int warp_kernel_ctas_per_sm(int mode, int m, int stages, int warps_per_cta, bool
 // final 2x2 (rank 0's F.a and rank world-1's L.c are zero), then walk the
 // chain back down to this rank.
 // ---------------------------------------------------------------------------
+// Peer-memory exchange (NVLink P2P) of the interface equations, replacing
+// the all-gather.  Every rank owns an exchange buffer laid out as
+//   [2 parities][world][8] reals  |  [2 parities][world] uint64 epochs
+// (pm_dist_exchange_bytes).  Publish: rank r stores its 8 reals into slot
+// [epoch & 1][r] of every peer's buffer, then a system-scope fence and a
+// release store of the epoch into the peer's flag [epoch & 1][r].  The solve
+// side (dist_chain_kernel with flags) spins on acquire loads of its own flags
+// until every rank's epoch arrived.  Two parities: a rank can run ahead by
+// one solve only (its next publish needs every peer's current publish).
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void dist_publish_kernel(const real* __restrict__ iface, void* const* __restrict__ peers,
+                                    int world, int rank, uint64_t epoch) {
+  const int k = threadIdx.x;  // destination rank
+  if (k >= world) return;
+  const int par = static_cast<int>(epoch & 1);
+  real* slots = static_cast<real*>(peers[k]);
+  uint64_t* flags = reinterpret_cast<uint64_t*>(slots + (size_t)2 * world * 8);
+  real* dst = slots + ((size_t)par * world + rank) * 8;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) dst[j] = iface[j];
+  __threadfence_system();
+  st_release_sys(flags + par * world + rank, epoch);
+}
+
+cudaError_t launch_dist_publish(const real* iface, void* const* peers, int world, int rank,
+                                uint64_t epoch, cudaStream_t st) {
+  dist_publish_kernel<<<1, ((world + 31) / 32) * 32, 0, st>>>(iface, peers, world, rank, epoch);
+  return cudaGetLastError();
+}
+
 __global__ void dist_chain_kernel(const real* __restrict__ iface, int world, int rank,
-                                  real* __restrict__ xb, int* flag) {
+                                  real* __restrict__ xb, int* flag, const uint64_t* flags,
+                                  uint64_t epoch, uint64_t timeout_ns) {
   extern __shared__ Node chain_nodes[];
   if (threadIdx.x != 0) return;
   bool bad = false;
+  if (flags) {  // P2P exchange: wait for every rank's interface equations
+    const int par = static_cast<int>(epoch & 1);
+    const uint64_t t0 = global_ns();
+    for (int k = 0; k < world; ++k) {
+      while (ld_acquire_sys(flags + par * world + k) < epoch) {
+        if (global_ns() - t0 > timeout_ns) {  // a peer never published
+          atomicOr(flag, 4);
+          return;
+        }
+        __nanosleep(256);
+      }
+    }
+    iface += (size_t)par * world * 8;
+  }
   // per rank: [Fa, La, Fb, Lb, Fc, Lc, Fd, Ld] (the REDUCE kernel's output
   // layout for a one-tile level: ra = p, rb = p + 2, rc = p + 4, rd = p + 6)
   auto seg_of = [&](int k) {
@@ -778,10 +836,11 @@ __global__ void dist_chain_kernel(const real* __restrict__ iface, int world, int
 }
 
 cudaError_t launch_dist_chain(const real* iface_all, int world, int rank, real* xb, int* flag,
-                              cudaStream_t st) {
+                              cudaStream_t st, const uint64_t* flags, uint64_t epoch,
+                              uint64_t timeout_ns) {
   const size_t smem = (size_t)world * sizeof(Node);
   if (smem > 48 * 1024) return cudaErrorInvalidValue;
-  dist_chain_kernel<<<1, 32, smem, st>>>(iface_all, world, rank, xb, flag);
+  dist_chain_kernel<<<1, 32, smem, st>>>(iface_all, world, rank, xb, flag, flags, epoch, timeout_ns);
   return cudaGetLastError();
 }
 

@@ -36,9 +36,20 @@ def row_offset(n: int, world: int, m: int, rank: int) -> int:
 
 class DistributedSolver:
     """Collective row-sharded solve over an initialised torch.distributed group
-    (backend nccl on GPUs; every rank calls `solve`)."""
+    (every rank calls `solve`).
 
-    def __init__(self, solver, group=None, device=None):
+    exchange="p2p" (default when it works): the interface equations travel
+    through peer memory -- every rank's exchange buffer is mapped into every
+    other rank with CUDA IPC (NVLink), pm_dist_reduce_p2p publishes this
+    rank's 64 bytes into every peer and pm_dist_solve_p2p waits on the peers'
+    epoch flags inside the solve kernel: no collective call and no host sync
+    on the data path.  torch.distributed only carries the one-time handle
+    exchange (and the self-test that validates the mapping).
+    exchange="collective": all_gather_into_tensor of the 8 doubles per rank
+    (NCCL over NVLink; gloo stages through the host).
+    """
+
+    def __init__(self, solver, group=None, device=None, exchange: str = "auto"):
         import torch
         import torch.distributed as dist
 
@@ -50,6 +61,49 @@ class DistributedSolver:
         dev = device if device is not None else torch.device("cuda", solver.device)
         self.iface = torch.zeros(8, dtype=torch.float64, device=dev)
         self.iface_all = torch.zeros(8 * self.world, dtype=torch.float64, device=dev)
+        self._opened = []
+        self.exchange = "collective"
+        if exchange in ("auto", "p2p"):
+            try:
+                self._setup_p2p()
+                self.exchange = "p2p"
+            except Exception:
+                if exchange == "p2p":
+                    raise
+
+    def _setup_p2p(self):
+        """Map every rank's exchange buffer (CUDA IPC) and register them."""
+        import torch
+
+        from .solver import ipc_get_handle, ipc_open_handle
+
+        own = self.solver.dist_exchange_alloc(self.world)
+        h = torch.frombuffer(bytearray(ipc_get_handle(own)), dtype=torch.uint8)
+        if self.dist.get_backend(self.group) == "nccl":
+            hs = [torch.empty(64, dtype=torch.uint8, device=self.iface.device) for _ in range(self.world)]
+            self.dist.all_gather(hs, h.to(self.iface.device), group=self.group)
+            hs = [t.cpu() for t in hs]
+        else:
+            hs = [torch.empty(64, dtype=torch.uint8) for _ in range(self.world)]
+            self.dist.all_gather(hs, h, group=self.group)
+        ptrs = []
+        for k, hk in enumerate(hs):
+            if k == self.rank:
+                ptrs.append(own)
+            else:
+                p = ipc_open_handle(bytes(hk.numpy().tobytes()))
+                self._opened.append(p)
+                ptrs.append(p)
+        self.solver.dist_set_peers(ptrs, self.rank)
+        # self-test: one exchange of tiny systems through the mapping
+        dt = torch.float64
+        n = 40
+        t = [torch.full((n,), v, dtype=dt, device=self.iface.device) for v in (0.5, 4.0, 0.5, 1.0)]
+        x = torch.empty(n, dtype=dt, device=self.iface.device)
+        self.solver.dist_reduce_p2p(*t, m=10)
+        self.solver.dist_solve_p2p(*t, x, m=10)
+        self.solver.check()
+        self.dist.barrier(group=self.group)
 
     def _all_gather(self):
         if self.iface.is_cuda and self.dist.get_backend(self.group) != "nccl":
@@ -59,6 +113,13 @@ class DistributedSolver:
             self.iface_all.copy_(hall)
         else:
             self.dist.all_gather_into_tensor(self.iface_all, self.iface, group=self.group)
+
+    def close(self):
+        from .solver import ipc_close_handle
+
+        for p in self._opened:
+            ipc_close_handle(p)
+        self._opened = []
 
     def solve_host(self, a, b, c, d, x, m: int = 10, stream=None):
         """End-to-end collective solve from this rank's host rows (page-locked
@@ -90,6 +151,10 @@ class DistributedSolver:
         return x
 
     def solve(self, a, b, c, d, x, m: int = 10, stream=None):
+        if self.exchange == "p2p":
+            self.solver.dist_reduce_p2p(a, b, c, d, m, stream=stream)
+            self.solver.dist_solve_p2p(a, b, c, d, x, m, stream=stream)
+            return x
         if self.iface.dtype != b.dtype:  # FP32 solve: interface equations in FP32
             self.iface = self.iface.to(b.dtype)
             self.iface_all = self.iface_all.to(b.dtype)

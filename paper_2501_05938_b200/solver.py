@@ -252,6 +252,29 @@ class PartitionSolver:
                     _dev_ptr(x, n, dt), n, m, rank, world, _dev_ptr(iface_all, 8 * world, dt),
                     _stream_handle(stream)))
 
+    # -- P2P interface exchange (NVLink peer memory; include/pm_tridiag.h) -------
+    def dist_exchange_alloc(self, world: int) -> int:
+        """This rank's exchange buffer (device pointer, owned by the handle)."""
+        out = C.c_void_p()
+        self._ok(self._L.pm_dist_exchange_alloc(self._h, int(world), C.byref(out)))
+        return int(out.value)
+
+    def dist_set_peers(self, peer_ptrs, rank: int):
+        arr = (C.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+        self._ok(self._L.pm_dist_set_peers(self._h, arr, len(peer_ptrs), int(rank)))
+
+    def dist_reduce_p2p(self, a, b, c, d, m: int, stream=None):
+        n, dt = int(b.numel()), b.dtype
+        fn = getattr(self._L, "pm_dist_reduce_p2p_" + _suffix(dt))
+        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt), n,
+                    m, _stream_handle(stream)))
+
+    def dist_solve_p2p(self, a, b, c, d, x, m: int, stream=None):
+        n, dt = int(b.numel()), b.dtype
+        fn = getattr(self._L, "pm_dist_solve_p2p_" + _suffix(dt))
+        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
+                    _dev_ptr(x, n, dt), n, m, _stream_handle(stream)))
+
     # -- stream-count model -------------------------------------------------------
     def set_model_bundle(self, bundle: "ModelBundleC"):
         self._ok(self._L.pm_set_model_bundle(self._h, C.byref(bundle)))
@@ -260,6 +283,25 @@ class PartitionSolver:
         b = _lib.ModelBundleC()
         self._ok(self._L.pm_get_model_bundle(self._h, C.byref(b)))
         return b
+
+
+def ipc_get_handle(dptr: int) -> bytes:
+    """CUDA IPC handle (64 bytes) of a cudaMalloc'd device pointer."""
+    buf = C.create_string_buffer(64)
+    if _lib.load().pm_ipc_get_handle(C.c_void_p(dptr), buf) != 0:
+        raise CudaRuntimeError("cudaIpcGetMemHandle failed")
+    return buf.raw
+
+
+def ipc_open_handle(handle: bytes) -> int:
+    out = C.c_void_p()
+    if _lib.load().pm_ipc_open_handle(C.c_char_p(bytes(handle)), C.byref(out)) != 0:
+        raise CudaRuntimeError("cudaIpcOpenMemHandle failed")
+    return int(out.value)
+
+
+def ipc_close_handle(dptr: int) -> None:
+    _lib.load().pm_ipc_close_handle(C.c_void_p(dptr))
 
 
 def pinned_empty(n: int, dtype=np.float64) -> np.ndarray:

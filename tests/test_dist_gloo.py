@@ -87,7 +87,7 @@ def _worker(rank, world, port, n, m, q):
         rows = split_rows(n, world, m)
         off = row_offset(n, world, m, rank)
         a, b, c, d = (torch.from_numpy(v[off:off + rows[rank]].copy()) for v in oracle.generate(n, 5))
-        ds = DistributedSolver(NumpyDistBackend(), device=torch.device("cpu"))
+        ds = DistributedSolver(NumpyDistBackend(), device=torch.device("cpu"), exchange="collective")
         x = torch.empty(rows[rank], dtype=torch.float64)
         ds.solve(a, b, c, d, x, m=m)
         mx = max(rows)

@@ -342,6 +342,60 @@ def test_dist_virtual_ranks(solver, world, n, m):
     _check(torch.cat(xs).cpu().numpy(), ah, bh, ch, dh)
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("n,m", [(1_000_000, 10), (77_777, 7)])
+def test_dist_p2p_virtual_ranks(solver, world, n, m):
+    """The P2P exchange (pm_dist_reduce_p2p / pm_dist_solve_p2p) with `world`
+    handles in one process: every rank's exchange buffer is a plain device
+    pointer here (CUDA IPC maps it across processes; see the bench test)."""
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.dist import split_rows
+
+    handles = [solver] + [PartitionSolver(0) for _ in range(world - 1)]
+    bufs = [h.dist_exchange_alloc(world) for h in handles]
+    for r, h in enumerate(handles):
+        h.dist_set_peers(bufs, r)
+    ah, bh, ch, dh = oracle.generate(n, 23)
+    rows = split_rows(n, world, m)
+    offs = np.concatenate([[0], np.cumsum(rows)])
+    loc = [[torch.from_numpy(v[offs[r]:offs[r + 1]].copy()).cuda() for v in (ah, bh, ch, dh)]
+           for r in range(world)]
+    for rep in range(3):  # consecutive solves: epochs and both buffer parities
+        for r in range(world):
+            handles[r].dist_reduce_p2p(*loc[r], m=m)
+        xs = []
+        for r in range(world):
+            x = torch.empty(rows[r], dtype=torch.float64, device="cuda")
+            handles[r].dist_solve_p2p(*loc[r], x, m=m)
+            xs.append(x)
+        for h in handles:
+            h.check()
+        _check(torch.cat(xs).cpu().numpy(), ah, bh, ch, dh)
+    for h in handles[1:]:
+        h.close()
+
+
+def test_dist_p2p_timeout_is_runtime_error(solver):
+    """A peer that never publishes: the wait gives up (20 s) with PM_ERR_RUNTIME."""
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver, errors
+
+    other = PartitionSolver(0)
+    bufs = [solver.dist_exchange_alloc(2), other.dist_exchange_alloc(2)]
+    solver.dist_set_peers(bufs, 0)
+    other.dist_set_peers(bufs, 1)
+    a, b, c, d = (torch.from_numpy(v).cuda() for v in oracle.generate(1000, 1))
+    solver.dist_reduce_p2p(a, b, c, d, m=10)  # rank 1 never reduces
+    x = torch.empty(1000, dtype=torch.float64, device="cuda")
+    solver.dist_solve_p2p(a, b, c, d, x, m=10)
+    with pytest.raises(errors.CudaRuntimeError):
+        solver.check()
+    other.close()
+
+
 def test_validation_errors(solver):
     import torch
 
@@ -465,8 +519,9 @@ def test_golden_scaled_systems(solver):
             assert oracle.rel_err(x.cpu().numpy(), xg) <= REL_TOL, (key, m)
 
 
+@pytest.mark.parametrize("exchange", ["collective", "p2p"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_bench_row_sharded_path(world, tmp_path):
+def test_bench_row_sharded_path(world, exchange, tmp_path):
     """bench.py's multi-rank path (DistributedSolver: reduce -> all_gather ->
     solve) with `world` processes sharing cuda:0 over gloo, checked against the
     oracle.  (The NCCL run needs one GPU per rank.)"""
@@ -477,13 +532,14 @@ def test_bench_row_sharded_path(world, tmp_path):
 
     root = Path(__file__).resolve().parents[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), str(root / "bench.py"),
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world + (20 if exchange == "p2p" else 0)), str(root / "bench.py"),
            "--gpus", str(world), "--steps", "3", "--warmup", "3", "--rows-per-gpu", "333337",
-           "--dist-backend", "gloo", "--same-device", "--e2e-steps", "2", "--check"]
+           "--dist-backend", "gloo", "--same-device", "--e2e-steps", "2", "--check", "--exchange", exchange]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == world and line["check"]["rel_err"] <= REL_TOL
+    assert line["config"]["exchange"] == exchange
     assert line["check"]["residual"] <= RES_TOL
     # the end-to-end path (DistributedSolver.solve_host from pinned host rows)
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 32 * 333337 * world
