@@ -210,7 +210,7 @@ def run_batch(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
-    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200 import PartitionSolver, pinned_empty
     from paper_2501_05938_b200.solver import PM_OPT_KERNEL_TIMES
 
     nps, m = args.batch_rows, args.m
@@ -239,6 +239,7 @@ def run_batch(args, world, rank, local):
             step()
     solver.check()
     plan = solver.last_batch_plan()
+    launches_per_step = solver.last_launch_count
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -267,6 +268,37 @@ def run_batch(args, world, rank, local):
         ms = float(t.item())
     ms_per_step = ms / args.steps
     n_total = args.batch * nps
+    # e2e: pm_solve_batch_host_f64 from pinned host rows (chunked H2D / solve /
+    # D2H on three streams), max over ranks
+    e2e = None
+    if not args.no_e2e:
+        try:
+            host = [pinned_empty(n_loc) for _ in range(5)]
+        except RuntimeError:
+            host = None
+        if host is not None:
+            for hbuf, t in zip(host, (a, b, c, d)):
+                torch.from_numpy(hbuf).copy_(t)
+            del a, b, c, d
+            torch.cuda.empty_cache()
+            solver.solve_batch_host(*host[:4], n_per_system=nps, m=m, out=host[4])  # warm-up
+            times = []
+            for _ in range(args.e2e_steps):
+                if world > 1:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                solver.solve_batch_host(*host[:4], n_per_system=nps, m=m, out=host[4])
+                times.append(time.perf_counter() - t0)
+            t_e2e = statistics.median(times)
+            if world > 1:
+                t = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                t_e2e = float(t.item())
+            e2e = {"value": n_total / t_e2e, "unit": "unknowns/s", "h2d_bytes_per_step": 32 * n_total,
+                   "d2h_bytes_per_step": 8 * n_total, "ms_per_step": t_e2e * 1e3,
+                   "link_gbs_per_gpu": 40 * n_loc / t_e2e / 1e9, "steps": args.e2e_steps,
+                   "timing": "host wall clock around pm_solve_batch_host_f64 (3 streams, chunks of "
+                             "~64 MB), median, max over ranks"}
     value = n_total * args.steps / (ms / 1e3)
     peak, peak_src = peaks()
     if plan["cluster"]:
@@ -308,9 +340,9 @@ def run_batch(args, world, rank, local):
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                          "traffic": traffic, "kernel": kname, "peak_source": peak_src, "kernel_ms": kms,
                          "whole_step": {"achieved": whole, "frac": whole / peak, "bytes_per_unknown": bpu}},
-            "e2e": None,
+            "e2e": e2e,
             "cpu_baseline": None,
-            "gpu_launches": args.steps * (1 if plan["cluster"] else 5),
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -135,6 +135,19 @@ int pm_solve_batch_device_f64(pm_handle_t h, const double* a, const double* b, c
  * zero when the last batch solve used the level kernels. */
 int pm_last_batch_plan(pm_handle_t h, int32_t* out6);
 
+/* Batch of independent systems from host memory, end to end (config 4):
+ * chunks of `systems_per_chunk` systems (0 = ~64 MB of inputs per chunk) flow
+ * H2D -> batch solve -> D2H through a ring of `depth` device staging slots
+ * (0 = 3) on separate copy-in / compute / copy-out streams, so the copy-in of
+ * one chunk overlaps the copy-out of an earlier one (PCIe is full duplex).
+ * Synchronous; page-locked host arrays required for the overlap. */
+int pm_solve_batch_host_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                            const double* d, double* x, int64_t n_per_system, int64_t batch, int32_t m,
+                            int32_t depth, int64_t systems_per_chunk);
+int pm_solve_batch_host_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                            const float* d, float* x, int64_t n_per_system, int64_t batch, int32_t m,
+                            int32_t depth, int64_t systems_per_chunk);
+
 /* Waits for the handle's last stream; PM_ERR_COMPUTATION if any solve since
  * the previous check met a zero or non-finite pivot (the flag is cleared). */
 int pm_check(pm_handle_t h);

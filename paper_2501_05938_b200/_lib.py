@@ -70,6 +70,10 @@ PM_SIGNATURES = [
      [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),
     ("pm_dist_solve_f32", C.c_int,
      [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _CD, C.c_void_p]),
+    ("pm_solve_batch_host_f64", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int64]),
+    ("pm_solve_batch_host_f32", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int64]),
     # P2P interface exchange
     ("pm_dist_exchange_bytes", C.c_int64, [C.c_int32]),
     ("pm_dist_exchange_alloc", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),

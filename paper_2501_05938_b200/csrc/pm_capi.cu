@@ -835,6 +835,115 @@ int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   return PM_OK;
 }
 
+// ---- batch of independent systems from host memory (config 4 end to end) --
+// Chunks of whole systems flow through a ring of `depth` device staging
+// slots: H2D of chunk k on the copy-in stream, the batch solve of chunk k on
+// the main stream (chunks serialised there: they share the level scratch),
+// D2H of chunk k on the copy-out stream.  PCIe is full duplex, so the
+// copy-in of chunk k+1 overlaps the copy-out of chunk k-1: e2e time tends to
+// max(H2D, D2H) instead of their sum (a single system cannot do this: its
+// Stage 3 needs all of Stage 1).
+template <class R>
+int solve_batch_host_impl(pm_handle_t h, const R* a, const R* b, const R* c, const R* d, R* x,
+                          int64_t n_per_system, int64_t batch, int32_t m, int32_t depth,
+                          int64_t systems_per_chunk) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (batch < 1 || n_per_system < 1) return fail(h, PM_ERR_VALIDATION, "batch and n_per_system must be >= 1");
+  if (n_per_system > INT64_MAX / batch) return fail(h, PM_ERR_VALIDATION, "batch too large");
+  int r = validate_common(h, a, b, c, d, x, n_per_system * batch, m);
+  if (r) return r;
+  if (depth == 0) depth = 3;
+  if (depth < 1 || depth > 32) return fail(h, PM_ERR_VALIDATION, "depth must lie in [1, 32] (0 = 3)");
+  if (systems_per_chunk <= 0)  // ~64 MB of a, b, c, d per chunk
+    systems_per_chunk = std::max<int64_t>(1, ((int64_t)64 << 20) / (4 * (int64_t)sizeof(R) * n_per_system));
+  systems_per_chunk = std::min<int64_t>(systems_per_chunk, batch);
+  const int64_t nchunks = (batch + systems_per_chunk - 1) / systems_per_chunk;
+  depth = (int)std::min<int64_t>(depth, nchunks);
+  PM_CUDA(h, cudaSetDevice(h->device));
+  const int64_t rows = systems_per_chunk * n_per_system;
+  const size_t stride = (size_t)((rows + 31) / 32 * 32);
+  const size_t need = (size_t)depth * 5 * stride * sizeof(R);
+  if (need > h->hbuf_bytes) {
+    if (h->hbuf) {
+      PM_CUDA(h, cudaDeviceSynchronize());
+      PM_CUDA(h, cudaFree(h->hbuf));
+      h->hbuf = nullptr;
+      h->hbuf_bytes = 0;
+    }
+    PM_CUDA(h, cudaMalloc(&h->hbuf, need));
+    h->hbuf_bytes = need;
+  }
+  while ((int)h->pool.size() < 2) {
+    cudaStream_t sn;
+    PM_CUDA(h, cudaStreamCreateWithFlags(&sn, cudaStreamNonBlocking));
+    h->pool.push_back(sn);
+  }
+  cudaStream_t s_in = h->pool[0], s_out = h->pool[1], s_comp = h->main;
+  std::vector<cudaEvent_t> evs;
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  };
+  auto mk = [&](cudaEvent_t* e) {
+    cudaError_t err = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    if (err == cudaSuccess) evs.push_back(*e);
+    return err;
+  };
+  std::vector<cudaEvent_t> in_done(depth), comp_done(depth), out_done(depth);
+  for (int k = 0; k < depth; ++k) {
+    cudaError_t e1 = mk(&in_done[k]), e2 = mk(&comp_done[k]), e3 = mk(&out_done[k]);
+    if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+      cleanup();
+      return cuda_fail(h, e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3), "cudaEventCreate");
+    }
+  }
+  cudaEvent_t start;
+  if (mk(&start) != cudaSuccess) { cleanup(); return cuda_fail(h, cudaErrorUnknown, "cudaEventCreate"); }
+  // order the three streams after everything the caller enqueued before
+  cudaEventRecord(start, s_comp);
+  cudaStreamWaitEvent(s_in, start, 0);
+  cudaStreamWaitEvent(s_out, start, 0);
+  int launches = 0;
+  cudaError_t e = cudaSuccess;
+  for (int64_t k = 0; k < nchunks && e == cudaSuccess; ++k) {
+    const int slot = (int)(k % depth);
+    const int64_t s0 = k * systems_per_chunk;
+    const int64_t ns = std::min<int64_t>(systems_per_chunk, batch - s0);
+    const int64_t r0 = s0 * n_per_system, nr = ns * n_per_system;
+    R* base = reinterpret_cast<R*>(h->hbuf) + (size_t)slot * 5 * stride;
+    R* da = base;
+    R* db = base + stride;
+    R* dc = base + 2 * stride;
+    R* dd = base + 3 * stride;
+    R* dx = base + 4 * stride;
+    const size_t bytes = (size_t)nr * sizeof(R);
+    if (k >= depth) cudaStreamWaitEvent(s_in, out_done[slot], 0);  // slot free again
+    if (e == cudaSuccess) e = cudaMemcpyAsync(da, a + r0, bytes, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(db, b + r0, bytes, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dc, c + r0, bytes, cudaMemcpyHostToDevice, s_in);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dd, d + r0, bytes, cudaMemcpyHostToDevice, s_in);
+    cudaEventRecord(in_done[slot], s_in);
+    cudaStreamWaitEvent(s_comp, in_done[slot], 0);
+    if (e != cudaSuccess) break;
+    if ((r = solve_batch_impl<R>(h, da, db, dc, dd, dx, n_per_system, ns, m, s_comp))) {
+      cleanup();
+      return r;
+    }
+    launches += h->launches;
+    cudaEventRecord(comp_done[slot], s_comp);
+    cudaStreamWaitEvent(s_out, comp_done[slot], 0);
+    e = cudaMemcpyAsync(x + r0, dx, bytes, cudaMemcpyDeviceToHost, s_out);
+    cudaEventRecord(out_done[slot], s_out);
+  }
+  if (e != cudaSuccess) { cleanup(); return cuda_fail(h, e, "cudaMemcpyAsync"); }
+  cudaError_t se = cudaStreamSynchronize(s_out);
+  if (se == cudaSuccess) se = cudaStreamSynchronize(s_comp);
+  cleanup();
+  if (se != cudaSuccess) return cuda_fail(h, se, "batch solve");
+  h->launches = launches;
+  h->last_stream = s_comp;
+  return read_flag(h, s_comp);
+}
+
 // ---- P2P interface exchange (NVLink peer memory instead of the all-gather) --
 
 size_t exchange_bytes(int world) {
@@ -1134,6 +1243,17 @@ int pm_dist_solve_f32(pm_handle_t h, const float* a, const float* b, const float
                       const float* d, float* x, int64_t n_local, int32_t m, int32_t rank,
                       int32_t world, const float* iface_all, void* stream) {
   return dist_solve_impl<float>(h, a, b, c, d, x, n_local, m, rank, world, iface_all, stream);
+}
+
+int pm_solve_batch_host_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                            const double* d, double* x, int64_t n_per_system, int64_t batch, int32_t m,
+                            int32_t depth, int64_t systems_per_chunk) {
+  return solve_batch_host_impl<double>(h, a, b, c, d, x, n_per_system, batch, m, depth, systems_per_chunk);
+}
+int pm_solve_batch_host_f32(pm_handle_t h, const float* a, const float* b, const float* c,
+                            const float* d, float* x, int64_t n_per_system, int64_t batch, int32_t m,
+                            int32_t depth, int64_t systems_per_chunk) {
+  return solve_batch_host_impl<float>(h, a, b, c, d, x, n_per_system, batch, m, depth, systems_per_chunk);
 }
 
 int64_t pm_dist_exchange_bytes(int32_t world) {

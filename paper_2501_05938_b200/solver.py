@@ -195,6 +195,23 @@ class PartitionSolver:
                     _dev_ptr(x, n, dt), n_per_system, n // n_per_system, m, _stream_handle(stream)))
         return x
 
+    def solve_batch_host(self, a, b, c, d, n_per_system: int, m: int = 10, depth: int = 0,
+                         systems_per_chunk: int = 0, out=None) -> np.ndarray:
+        """pm_solve_batch_host_f64 / _f32: a batch from host memory, chunked
+        H2D / solve / D2H overlapped on three streams (synchronous)."""
+        dt = b.dtype if isinstance(b, np.ndarray) else np.float64
+        sfx = _suffix(dt)
+        _check_host(a, b, c, d, dtype=dt)
+        n = b.shape[0]
+        if n_per_system < 1 or n % n_per_system:
+            raise ValidationError("array length must be a multiple of n_per_system")
+        x = out if out is not None else np.empty(n, dt)
+        _check_host(x, dtype=dt)
+        fn = getattr(self._L, "pm_solve_batch_host_" + sfx)
+        self._ok(fn(self._h, a.ctypes.data, b.ctypes.data, c.ctypes.data, d.ctypes.data, x.ctypes.data,
+                    n_per_system, n // n_per_system, m, depth, systems_per_chunk))
+        return x
+
     def check(self):
         """pm_check: synchronise and raise ComputationError on a pivot failure."""
         self._ok(self._L.pm_check(self._h))

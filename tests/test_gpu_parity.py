@@ -262,6 +262,37 @@ def test_batch_cluster_aliasing_and_zero_pivot(solver):
         solver.set_option(PM_OPT_BATCH_CLUSTER, 0)
 
 
+@pytest.mark.parametrize("depth,spc", [(0, 0), (1, 3), (2, 5), (3, 7), (4, 64)])
+def test_batch_host_pipeline(solver, depth, spc):
+    """pm_solve_batch_host_f64: chunked H2D / solve / D2H on three streams."""
+    from paper_2501_05938_b200 import pinned_empty
+
+    nps, batch = 20_000, 23
+    systems, cat = _batch_systems(nps, batch, 17)
+    host = [pinned_empty(nps * batch) for _ in range(5)]
+    for h, v in zip(host, cat):
+        h[:] = v
+    x = solver.solve_batch_host(*host[:4], n_per_system=nps, m=10, depth=depth, systems_per_chunk=spc,
+                                out=host[4])
+    for k, s in enumerate(systems):
+        _check(x[k * nps:(k + 1) * nps], *s)
+
+
+def test_batch_host_pipeline_f32_and_pageable(solver):
+    nps, batch = 5_000, 9
+    systems, cat = _batch_systems(nps, batch, 3)
+    c32 = [v.astype(np.float32) for v in cat]
+    x = solver.solve_batch_host(*c32, n_per_system=nps, m=10, systems_per_chunk=2)  # pageable
+    assert x.dtype == np.float32
+    for k in range(batch):
+        sl = slice(k * nps, (k + 1) * nps)
+        a, b, c, d = (v[sl].astype(np.float64) for v in c32)
+        a[0] = 0.0
+        c[-1] = 0.0
+        xr = oracle.thomas(a, b, c, d)
+        assert oracle.rel_err(x[sl].astype(np.float64), xr) <= 1e-5
+
+
 def test_batch_config4_sample(solver):
     """BASELINE config 4 on one GPU: 4096 x 1e5, sampled systems checked."""
     import torch
