@@ -95,8 +95,8 @@ typedef struct pm_model_bundle {
 #define PM_OPT_UPPER_M 11      /* rows per thread of the warp-tile upper levels
                                   (default 0 = CTA tiles with m = 8)               */
 #define PM_OPT_ROOT_M 12       /* ROOT tile = 128 * root_m rows (default 8)        */
-#define PM_OPT_PDL 13          /* 1 (default): launch with programmatic dependent
-                                  launch (process-wide setting)                    */
+#define PM_OPT_PDL 13          /* programmatic dependent launch (process-wide;
+                                  default: on for the FP64 kernels, off for FP32)  */
 #define PM_OPT_BATCH_CLUSTER 14 /* 1: pm_solve_batch_device_f64 runs one thread-
                                   block cluster per system (all stages while the
                                   system is L2-resident: 40 B/unknown of HBM
@@ -110,6 +110,9 @@ typedef struct pm_model_bundle {
 #define PM_OPT_BATCH_CLUSTER_SIZE 16 /* force CTAs per cluster, 1..8 (0 = plan)   */
 #define PM_OPT_BATCH_WARPS 17  /* force warps per CTA, 4..16 (0 = plan)           */
 #define PM_OPT_BATCH_STAGES 18 /* force bulk-copy stages per warp, 1..2 (0 = plan) */
+#define PM_OPT_PAIR_TILES 19   /* level-0 pair tiles (two m-blocks per lane, 64*m
+                                  rows per warp tile; m in {2, 8, 10, 16}):
+                                  -1 (default) = on for FP32, off for FP64; 0; 1  */
 
 int pm_create(pm_handle_t* out, int device);
 int pm_destroy(pm_handle_t h);

@@ -48,6 +48,7 @@ struct Level {
   int pad_mode = 1;
   int stages = 2;
   int warps_per_cta = 0;  // > 0: warp-tile kernel (P = 32 rows-blocks per tile)
+  bool pair = false;      // level-0 pair-tile kernel (P = 64, two blocks per lane)
 };
 
 constexpr size_t kSmemLimit = 226 * 1024;
@@ -79,6 +80,10 @@ struct Prec<double> {
   }
   static size_t tile_smem(int mode, int P, int m, int S) { return pm::tile_smem_bytes(mode, P, m, S); }
   static size_t warp_smem(int mode, int m, int S) { return pm::warp_smem_bytes(mode, m, S); }
+  static cudaError_t pair(int mode, const Args& a, int w, int sm, cudaStream_t st, int* g) {
+    return pm::launch_warp_pair_kernel(mode, a, w, sm, st, g);
+  }
+  static size_t pair_smem(int m) { return pm::pair_smem_bytes(m); }
   static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st,
                                 const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
     return pm::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
@@ -107,6 +112,10 @@ struct Prec<float> {
   }
   static size_t tile_smem(int mode, int P, int m, int S) { return pm32::tile_smem_bytes(mode, P, m, S); }
   static size_t warp_smem(int mode, int m, int S) { return pm32::warp_smem_bytes(mode, m, S); }
+  static cudaError_t pair(int mode, const Args& a, int w, int sm, cudaStream_t st, int* g) {
+    return pm32::launch_warp_pair_kernel(mode, a, w, sm, st, g);
+  }
+  static size_t pair_smem(int m) { return pm32::pair_smem_bytes(m); }
   static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st,
                                 const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
     return pm32::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
@@ -136,6 +145,7 @@ struct pm_handle_s {
   int warp_tiles = 1;
   int solve_stages = 1;   // level-0 Stage 3 ring depth (0 = same as `stages`)
   int warps_per_cta = 4;
+  int pair_tiles = -1;  // PM_OPT_PAIR_TILES: -1 auto (FP32 on, FP64 off)
   // batch cluster kernel
   int batch_cluster = 0;
   int batch_l2_mb = 64;
@@ -262,6 +272,18 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
     L0.stages = pick_stages<R>(h->stages, L0.P, m);
     if (Prec<R>::tile_smem(pm::kModeSolve, L0.P, m, 1) > kSmemLimit)
       return fail(h, PM_ERR_VALIDATION, "sub-system size m too large for shared memory");
+  }
+  // pair tiles: two m-blocks per lane, 64*m rows per warp tile (not with
+  // chain mode, whose chunks are cut in 32-block tiles)
+  const bool want_pair = h->pair_tiles > 0 || (h->pair_tiles < 0 && sizeof(R) == 4);
+  if (L0.warps_per_cta > 0 && want_pair && pm::m_is_specialised(m) && !(h->opt_chain && allow_chain)) {
+    const int W = (int)std::min<size_t>(2, kSmemLimit / Prec<R>::pair_smem(m));
+    if (W >= 1) {
+      L0.pair = true;
+      L0.P = 64;
+      L0.stages = 1;
+      L0.warps_per_cta = W;
+    }
   }
   L0.T = (int64_t)L0.P * m;
   L0.ntiles = (n + L0.T - 1) / L0.T;
@@ -393,7 +415,9 @@ int launch(pm_handle_t h, int mode, const typename Prec<R>::Args& A, const Level
   const size_t ev = h->krec.size() * 2;
   if (timed) cudaEventRecord(h->kev[ev], st);
   cudaError_t e;
-  if (L.warps_per_cta > 0 && mode != pm::kModeRoot)
+  if (L.pair && mode != pm::kModeRoot)
+    e = Prec<R>::pair(mode, A, L.warps_per_cta, h->sm_count, st, &grid);
+  else if (L.warps_per_cta > 0 && mode != pm::kModeRoot)
     e = Prec<R>::warp(mode, A, L.warps_per_cta, h->sm_count, st, &grid);
   else
     e = Prec<R>::tile(mode, A, L.P, L.bulk, h->sm_count, st, &grid);
@@ -1088,6 +1112,10 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
     case PM_OPT_BATCH_STAGES:
       if (value < 0 || value > 2) return fail(h, PM_ERR_VALIDATION, "batch stages must lie in [0, 2]");
       h->batch_force_stages = (int)value;
+      return PM_OK;
+    case PM_OPT_PAIR_TILES:
+      if (value < -1 || value > 1) return fail(h, PM_ERR_VALIDATION, "pair tiles is -1 (auto), 0 or 1");
+      h->pair_tiles = (int)value;
       return PM_OK;
     case PM_OPT_KERNEL_TIMES:
       h->ktimes = value ? 1 : 0;

@@ -32,7 +32,15 @@
 
 namespace PM_NS {
 
+// Programmatic dependent launch: on for the FP64 kernels, off for FP32, where
+// the early-launched dependents cost 20-35 % of the solve on B200 (round-1
+// sweep: FP32 N = 8e7 0.594 -> 0.573 ms without PDL, pair tiles 0.652 ->
+// 0.481 ms; FP64 within noise either way).
+#ifdef PM_REAL_F32
+bool g_use_pdl = false;
+#else
 bool g_use_pdl = true;
+#endif
 
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <class K>
@@ -650,6 +658,208 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     }
   }
   if (bad) atomicOr(args.flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Pair-tile kernel (level 0, compile-time m): a warp tile is 64 m-blocks =
+// 64*m rows, two adjacent blocks per lane.  Each lane reduces its two blocks
+// (two independent dependency chains in flight) and merges them with one
+// in-register combine, so the warp tree (5 levels over 32 lanes, executed by
+// every lane) is paid once per 2*m rows instead of once per m rows.  One
+// bulk-copy stage per warp holding the tile's rows (read in place as 16-byte
+// pairs); Stage 1 releases it after the two block sweeps, Stage 3 after the
+// coalesced x store.  Same TileArgs, same level plan (P = 64 blocks per tile).
+// ---------------------------------------------------------------------------
+__host__ __device__ size_t pair_smem_bytes(int m) {
+  const size_t T = (size_t)64 * m;
+  const size_t bytes = 4 * T * sizeof(real) + 31 * sizeof(Node) + 2 * kMaxStages * sizeof(uint64_t);
+  return (bytes + 127) / 128 * 128;
+}
+
+#ifndef PM_PAIR_MINB
+#define PM_PAIR_MINB 5
+#endif
+template <int M, int MODE>
+__global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs args) {
+  static_assert(M > 0, "compile-time m only");
+  constexpr int T = 64 * M;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int r0 = lane * 2 * M;  // this lane's two blocks: rows [r0, r0 + M), [r0 + M, r0 + 2M)
+  const size_t per_warp = pair_smem_bytes(M);
+  unsigned char* base = smem_raw + per_warp * warp;
+  real* sa = reinterpret_cast<real*>(base);
+  real* sb = sa + T;
+  real* sc = sb + T;
+  real* sd = sc + T;
+  Node* nodes = reinterpret_cast<Node*>(sd + T);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + per_warp - 2 * kMaxStages * sizeof(uint64_t));
+
+  const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  const int64_t nwarp_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t ntiles = args.tile_end - args.tile_begin;
+  const int64_t nlocal = (ntiles > gwarp) ? (ntiles - gwarp + nwarp_total - 1) / nwarp_total : 0;
+  auto tile_of = [&](int64_t k) -> int64_t {
+    const int64_t idx = gwarp + k * nwarp_total;
+    return args.reverse ? (args.tile_end - 1 - idx) : (args.tile_begin + idx);
+  };
+  auto issue = [&](int64_t t) {
+    const int64_t row0 = t * T;
+    const int64_t v = (args.n - row0 < T) ? (args.n - row0) : T;
+    const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(kBulkRows - 1)) * sizeof(real));
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, 4u * bytes);
+    if (bytes) {
+      bulk_g2s(sa, args.a + row0, bytes, bar);
+      bulk_g2s(sb, args.b + row0, bytes, bar);
+      bulk_g2s(sc, args.c + row0, bytes, bar);
+      bulk_g2s(sd, args.d + row0, bytes, bar);
+    }
+  };
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  pdl_launch_dependents();
+  pdl_wait();
+  if (lane == 0 && nlocal > 0) issue(tile_of(0));
+
+  bool bad = false;
+  real xf_next = 0.0, xl_next = 0.0;
+  if (MODE != kModeReduce && nlocal > 0) {
+    const int64_t t0 = tile_of(0);
+    xf_next = __ldg(args.xb + 2 * t0);
+    xl_next = __ldg(args.xb + 2 * t0 + 1);
+  }
+  for (int64_t k = 0; k < nlocal; ++k) {
+    const int64_t t = tile_of(k);
+    const real xf_tile = xf_next, xl_tile = xl_next;
+    if (MODE != kModeReduce && k + 1 < nlocal) {
+      const int64_t tn = tile_of(k + 1);
+      xf_next = __ldg(args.xb + 2 * tn);
+      xl_next = __ldg(args.xb + 2 * tn + 1);
+    }
+    TileCtx ctx;
+    ctx.ga = args.a; ctx.gb = args.b; ctx.gc = args.c; ctx.gd = args.d;
+    ctx.row0 = t * T;
+    ctx.n = args.n;
+    ctx.valid = static_cast<int>((args.n - ctx.row0 < T) ? (args.n - ctx.row0) : T);
+    ctx.bulk_rows = ctx.valid & ~(kBulkRows - 1);
+    ctx.zf = args.zero_first != 0;
+    ctx.zl = args.zero_last != 0;
+    ctx.sys_len = args.sys_len;
+    // non-empty lanes (a prefix) and whether this lane's second block is non-empty
+    const int nblocks = args.pad_mode ? 64 : (ctx.valid + M - 1) / M;
+    const int nlanes = (nblocks + 1) / 2;
+    const bool has2 = 2 * lane + 1 < nblocks;
+    mbar_wait(bar, static_cast<uint32_t>(k & 1));
+
+    SmemAcc acc0{sa + r0, sb + r0, sc + r0, sd + r0, nullptr};
+    SmemAcc acc1{sa + r0 + M, sb + r0 + M, sc + r0 + M, sd + r0 + M, nullptr};
+    acc0.fixup(r0, M, ctx);
+    acc1.fixup(r0 + M, M, ctx);
+    const PairAcc<M> p0{sa + r0, sb + r0, sc + r0, sd + r0};
+    const PairAcc<M> p1{sa + r0 + M, sb + r0 + M, sc + r0 + M, sd + r0 + M};
+    const Seg s0 = block_reduce_fast<M, false>(p0, bad);
+    const Seg s1 = block_reduce_fast<M, false>(p1, bad);
+    Seg seg = s0;
+    Node lnode{};
+    if (has2) combine(s0, s1, seg, lnode, bad);
+    if constexpr (MODE == kModeReduce) {
+      __syncwarp();
+      if (lane == 0 && k + 1 < nlocal) issue(tile_of(k + 1));  // stage released
+      const Seg top = warp_upsweep(seg, nullptr, lane, nlanes, bad);
+      if (lane == 0) {
+        args.ra[2 * t] = top.F.a; args.rb[2 * t] = top.F.b;
+        args.rc[2 * t] = top.F.c; args.rd[2 * t] = top.F.d;
+        args.ra[2 * t + 1] = top.L.a; args.rb[2 * t + 1] = top.L.b;
+        args.rc[2 * t + 1] = top.L.c; args.rd[2 * t + 1] = top.L.d;
+      }
+    } else {
+      warp_upsweep(seg, nodes, lane, nlanes, bad);
+      real xf = xf_tile, xl = xl_tile;
+      __syncwarp();
+      warp_downsweep(xf, xl, nodes, lane, nlanes);
+      // split the lane's pair: block 0 = [xf, x_last(0)], block 1 = [x_first(1), xl]
+      real xl0 = xl, xf1 = 0.0;
+      if (has2) split_node(lnode, xf, xl, xl0, xf1);
+      real xv0[M], xv1[M];
+      block_solve_pairs<M>(p0, xf, xl0, xv0, bad);
+      block_solve_pairs<M>(p1, xf1, xl, xv1, bad);
+      __syncwarp();
+      bad |= !all_finite<M>(xv0);
+      if (has2) bad |= !all_finite<M>(xv1);
+      if constexpr ((M % 2) == 0) {
+#pragma unroll
+        for (int j = 0; j < M / 2; ++j) {
+          reinterpret_cast<real2*>(sb + r0)[j] = make_real2(xv0[2 * j], xv0[2 * j + 1]);
+          reinterpret_cast<real2*>(sb + r0 + M)[j] = make_real2(xv1[2 * j], xv1[2 * j + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          sb[r0 + j] = xv0[j];
+          sb[r0 + M + j] = xv1[j];
+        }
+      }
+      __syncwarp();
+      real* gx = args.x + ctx.row0;
+      const int v = ctx.valid;
+      if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & (sizeof(real2) - 1)) == 0)) {
+        const real2* s2 = reinterpret_cast<const real2*>(sb);
+        real2* g2 = reinterpret_cast<real2*>(gx);
+        for (int i = lane; i < v / 2; i += 32) g2[i] = s2[i];
+      } else {
+        for (int i = lane; i < v; i += 32) gx[i] = sb[i];
+      }
+      __syncwarp();
+      if (lane == 0 && k + 1 < nlocal) issue(tile_of(k + 1));
+    }
+  }
+  if (bad) atomicOr(args.flag, 1);
+}
+
+template <int M, int MODE>
+static cudaError_t launch_pair_one(const TileArgs& args, int warps_per_cta, int sm_count,
+                                   cudaStream_t st, int* grid_out) {
+  auto kern = warp_pair_kernel<M, MODE>;
+  const size_t smem = pair_smem_bytes(M) * warps_per_cta;
+  static thread_local size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int64_t ntiles = args.tile_end - args.tile_begin;
+  int64_t grid = (int64_t)per_sm * sm_count;
+  if (args.max_ctas > 0 && grid > args.max_ctas) grid = args.max_ctas;
+  const int64_t need = (ntiles + warps_per_cta - 1) / warps_per_cta;
+  if (grid > need) grid = need;
+  if (grid_out) *grid_out = (int)grid;
+  if (grid <= 0) return cudaSuccess;
+  return launch_kernel(kern, (unsigned)grid, 32 * warps_per_cta, smem, st, args);
+}
+
+cudaError_t launch_warp_pair_kernel(int mode, const TileArgs& args, int warps_per_cta, int sm_count,
+                                    cudaStream_t st, int* grid_out) {
+  const bool red = mode == kModeReduce;
+#define PM_PAIR_CASE(MM)                                                                       \
+  return red ? launch_pair_one<MM, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)   \
+             : launch_pair_one<MM, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out)
+  switch (args.m) {
+    case 2: PM_PAIR_CASE(2);
+    case 8: PM_PAIR_CASE(8);
+    case 10: PM_PAIR_CASE(10);
+    case 16: PM_PAIR_CASE(16);
+    default: return cudaErrorInvalidValue;
+  }
+#undef PM_PAIR_CASE
 }
 
 template <int M, int MODE, bool CHAIN>

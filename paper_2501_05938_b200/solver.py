@@ -35,6 +35,7 @@ PM_OPT_BATCH_L2_MB = 15
 PM_OPT_BATCH_CLUSTER_SIZE = 16
 PM_OPT_BATCH_WARPS = 17
 PM_OPT_BATCH_STAGES = 18
+PM_OPT_PAIR_TILES = 19
 PM_MAX_M = 128
 
 

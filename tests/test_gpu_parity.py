@@ -575,3 +575,91 @@ def test_bench_row_sharded_path(world, exchange, tmp_path):
     # the end-to-end path (DistributedSolver.solve_host from pinned host rows)
     assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] == 32 * 333337 * world
     assert line["check"]["e2e"]["rel_err"] <= REL_TOL and line["check"]["e2e"]["residual"] <= RES_TOL
+
+
+@pytest.fixture
+def pair_solver(solver):
+    from paper_2501_05938_b200.solver import PM_OPT_PAIR_TILES
+
+    solver.set_option(PM_OPT_PAIR_TILES, 1)
+    yield solver
+    solver.set_option(PM_OPT_PAIR_TILES, -1)
+
+
+@pytest.mark.parametrize("n,m", [(1, 10), (641, 10), (1280, 10), (1281, 10), (1_234_567, 10), (99_999, 8),
+                                 (500_001, 2), (333_333, 16), (640, 10), (639, 10), (2_000_000, 7)])
+def test_pair_tiles(pair_solver, n, m):
+    """Level-0 pair-tile kernel (two m-blocks per lane) vs the oracle."""
+    a, b, c, d = _device_system(pair_solver, n, seed=n % 97)
+    x = pair_solver.solve_device(a, b, c, d, m=m)
+    pair_solver.check()
+    _check(x.cpu().numpy(), *(t.cpu().numpy() for t in (a, b, c, d)))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_pair_tiles_dist(pair_solver, world):
+    """Ragged (non-padded) pair tiles on the non-last ranks of a row-sharded solve."""
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.dist import split_rows
+    from paper_2501_05938_b200.solver import PM_OPT_PAIR_TILES
+
+    n, m = 1_000_037, 10
+    handles = [pair_solver] + [PartitionSolver(0) for _ in range(world - 1)]
+    for h in handles[1:]:
+        h.set_option(PM_OPT_PAIR_TILES, 1)
+    ah, bh, ch, dh = oracle.generate(n, 31)
+    rows = split_rows(n, world, m)
+    offs = np.concatenate([[0], np.cumsum(rows)])
+    loc = [[torch.from_numpy(v[offs[r]:offs[r + 1]].copy()).cuda() for v in (ah, bh, ch, dh)]
+           for r in range(world)]
+    iface_all = torch.zeros(8 * world, dtype=torch.float64, device="cuda")
+    for r in range(world):
+        handles[r].dist_reduce(*loc[r], m=m, rank=r, world=world, iface=iface_all[8 * r:8 * r + 8])
+    xs = []
+    for r in range(world):
+        x = torch.empty(rows[r], dtype=torch.float64, device="cuda")
+        handles[r].dist_solve(*loc[r], x, m=m, rank=r, world=world, iface_all=iface_all)
+        xs.append(x)
+    for h in handles:
+        h.check()
+    for h in handles[1:]:
+        h.close()
+    _check(torch.cat(xs).cpu().numpy(), ah, bh, ch, dh)
+
+
+@pytest.mark.parametrize("ns", [1, 4, 32])
+def test_pair_tiles_host_and_batch(pair_solver, ns):
+    import torch
+
+    from paper_2501_05938_b200 import pinned_empty
+
+    n = 3_000_001
+    a, b, c, d = oracle.generate(n, 5)
+    host = [pinned_empty(n) for _ in range(5)]
+    for h, v in zip(host, (a, b, c, d)):
+        h[:] = v
+    x = pair_solver.solve_host(*host[:4], m=10, num_streams=ns, out=host[4])
+    _check(x, a, b, c, d)
+    nps, batch = 10_000, 12
+    systems, cat = _batch_systems(nps, batch, ns)
+    t = [torch.from_numpy(v).cuda() for v in cat]
+    xb = pair_solver.solve_batch_device(*t, n_per_system=nps, m=10).cpu().numpy()
+    pair_solver.check()
+    for k, s in enumerate(systems):
+        _check(xb[k * nps:(k + 1) * nps], *s)
+
+
+def test_pair_tiles_f32(pair_solver):
+    import torch
+
+    n = 2_000_003
+    a, b, c, d = (v.astype(np.float32) for v in oracle.generate(n, 9))
+    t = [torch.from_numpy(v).cuda() for v in (a, b, c, d)]
+    x = pair_solver.solve_device(*t, m=10).cpu().numpy().astype(np.float64)
+    pair_solver.check()
+    a64, b64, c64, d64 = (v.astype(np.float64) for v in (a, b, c, d))
+    a64[0] = 0.0
+    c64[-1] = 0.0
+    assert oracle.rel_err(x, oracle.thomas(a64, b64, c64, d64)) <= 1e-5
