@@ -107,9 +107,11 @@ typedef struct pm_model_bundle {
                                   kernels (72 B/unknown, faster on B200 today:
                                   DESIGN.md §6)                                   */
 #define PM_OPT_BATCH_L2_MB 15  /* L2 budget for the systems in flight (default 64) */
-#define PM_OPT_BATCH_CLUSTER_SIZE 16 /* force CTAs per cluster, 1..8 (0 = plan)   */
+#define PM_OPT_BATCH_CLUSTER_SIZE 16 /* force CTAs per cluster, 1..16 (0 = plan)  */
 #define PM_OPT_BATCH_WARPS 17  /* force warps per CTA, 4..16 (0 = plan)           */
 #define PM_OPT_BATCH_STAGES 18 /* force bulk-copy stages per warp, 1..2 (0 = plan) */
+#define PM_OPT_UPPER_CTA_M 20  /* rows per thread of the CTA-tile upper levels (8) */
+#define PM_OPT_UPPER_CTA_P 21  /* threads per CTA tile of the upper levels (128)   */
 #define PM_OPT_PAIR_TILES 19   /* level-0 pair tiles (two m-blocks per lane, 64*m
                                   rows per warp tile; m in {2, 8, 10, 16}):
                                   -1 (default) = on for FP32, off for FP64; 0; 1  */

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(512, 1) batch_cluster_kernel(BatchArgs args) {
     if (warp == 0) {
       double xf = 0.0, xl = 0.0;
       if (lane == 0) {
-        Node cn[8];
+        Node cn[16];
         Seg acc = *cluster.map_shared_rank(&slot[p], 0);
         for (int q = 1; q < CL; ++q) combine(acc, *cluster.map_shared_rank(&slot[p], q), acc, cn[q], bad);
         // acc.F.a and acc.L.c multiply unknowns outside the system (zero)
@@ -287,6 +287,10 @@ cudaError_t launch_m(const BatchArgs& a0, const BatchPlan& pl, cudaStream_t st) 
   const size_t smem = batch_warp_bytes(M, pl.stages) * pl.warps + batch_cta_bytes(pl.kmax);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (pl.cluster > 8) {  // clusters of 9-16 CTAs are a B200 opt-in
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.clusters * pl.cluster);
   cfg.blockDim = dim3(32 * pl.warps);
@@ -314,7 +318,9 @@ int max_clusters(int cluster, int warps, int stages, int kmax) {
   const size_t smem = batch_warp_bytes(M, stages) * warps + batch_cta_bytes(kmax);
   int n = 0;
   if (smem <= 227 * 1024 &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+      (cluster <= 8 ||
+       cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cluster);
     cfg.blockDim = dim3(32 * warps);
@@ -362,7 +368,10 @@ int plan_batch(int m, int64_t n_sys, int64_t batch, int sm_count, int64_t l2_bud
   BatchPlan bp{};
   for (int S = 1; S <= 2; ++S) {
     if (force_stages > 0 && S != force_stages) continue;
-    for (int CL = 1; CL <= 8; ++CL) {
+    // 9-16 CTA clusters only when forced: on B200 they place at most 14 (2
+    // CTAs per SM) and measured slower (round 1: 8.2 ms at CL = 16 vs 6.1 ms
+    // at CL = 8 for 4096 x 1e5)
+    for (int CL = 1; CL <= (force_cluster > 8 ? 16 : 8); ++CL) {
       if (force_cluster > 0 && CL != force_cluster) continue;
       if (CL > nt) break;
       const int kmax = (int)((nt + CL - 1) / CL);

@@ -175,6 +175,8 @@ struct pm_handle_s {
   int opt_chain = 0;
   int upper_m = 0;   // warp-tile m of the upper levels (0: CTA tiles, m = 8)
   int root_m = 8;    // ROOT tile: 128 * root_m rows
+  int upper_cta_m = 8;    // CTA-tile upper levels: rows per thread
+  int upper_cta_p = 128;  // ... and threads per CTA tile
   std::vector<int64_t> part_chunks, part_base;
   void* chain_nodes = nullptr;
   // P2P interface exchange (pm_dist_*_p2p): this rank's exchange buffer,
@@ -329,14 +331,14 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
   // Upper levels: warp tiles of 32*upper_m rows while the level exceeds one
   // ROOT tile (128*root_m rows), then the ROOT; ragged ranks use CTA tiles
   // with m = 2.
-  const int m_up = ragged0 ? 2 : 8;
+  const int m_up = ragged0 ? 2 : h->upper_cta_m;
   while (lv.back().ntiles > 1) {
     const Level& prev = lv.back();
     Level U;
     U.n = 2 * prev.ntiles;
     U.pad_mode = ragged0 ? 0 : 1;
     U.bulk = true;
-    U.P = 128;
+    U.P = ragged0 ? 128 : h->upper_cta_p;
     if (!ragged0 && h->upper_m > 0) {
       U.m = h->root_m;
       if (U.n > (int64_t)128 * h->root_m && h->warp_tiles) {
@@ -1101,7 +1103,7 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       h->batch_l2_mb = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_CLUSTER_SIZE:
-      if (value < 0 || value > 8) return fail(h, PM_ERR_VALIDATION, "cluster size must lie in [0, 8]");
+      if (value < 0 || value > 16) return fail(h, PM_ERR_VALIDATION, "cluster size must lie in [0, 16]");
       h->batch_force_cluster = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_WARPS:
@@ -1112,6 +1114,15 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
     case PM_OPT_BATCH_STAGES:
       if (value < 0 || value > 2) return fail(h, PM_ERR_VALIDATION, "batch stages must lie in [0, 2]");
       h->batch_force_stages = (int)value;
+      return PM_OK;
+    case PM_OPT_UPPER_CTA_M:
+      if (value < 2 || value > 32) return fail(h, PM_ERR_VALIDATION, "upper CTA m must lie in [2, 32]");
+      h->upper_cta_m = (int)value;
+      return PM_OK;
+    case PM_OPT_UPPER_CTA_P:
+      if (value != 64 && value != 128 && value != 256)
+        return fail(h, PM_ERR_VALIDATION, "upper CTA threads must be 64, 128 or 256");
+      h->upper_cta_p = (int)value;
       return PM_OK;
     case PM_OPT_PAIR_TILES:
       if (value < -1 || value > 1) return fail(h, PM_ERR_VALIDATION, "pair tiles is -1 (auto), 0 or 1");

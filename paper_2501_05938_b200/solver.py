@@ -36,6 +36,8 @@ PM_OPT_BATCH_CLUSTER_SIZE = 16
 PM_OPT_BATCH_WARPS = 17
 PM_OPT_BATCH_STAGES = 18
 PM_OPT_PAIR_TILES = 19
+PM_OPT_UPPER_CTA_M = 20
+PM_OPT_UPPER_CTA_P = 21
 PM_MAX_M = 128
 
 
