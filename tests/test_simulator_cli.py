@@ -287,3 +287,23 @@ def test_cli_baseline_and_simulate(tmp_path):
     assert rc == 0 and out.startswith("slae_size,")
     rc, _, _ = run("bogus")
     assert rc == 1
+
+
+def test_reference_data_checksums():
+    """the embedded ReferenceData (Tables 1, 2, 4, 5 and tau of
+    /root/reference/PAPER.md, transcribed in csrc/streamtune/dataset.cpp) is
+    pinned by checksums taken at transcription time (the values themselves
+    are cross-checked against PAPER.md literals in test_streamtune.py)."""
+    import hashlib
+
+    pinned = {
+        "table1": "5ae56b65daaf9b0bb856aaf6ff9f98cdca761061f5eca26d992f66d32c15aa61",
+        "table2": "c8e38d21a1bcabf83590a4c285e50d8933e5b8d187f6aa887d5d8c10b05b019d",
+        "table4": "bc5a47d50445b9aade880334c68f8a340c1c5d3d8f67246c47f3ef9dcc6c43b8",
+        "table5": "2f360de02e62f49496a95ef74354e1505b49831ff5fbb8f7ccfb27f52438b53c",
+        "tau": "75bbd116ec994e2656babefec8c787a2361b9d15944f266b947801a5678e5c27",
+    }
+    for table, digest in pinned.items():
+        assert hashlib.sha256(st.dump_reference(table).encode()).hexdigest() == digest, table
+    t5 = st.dump_reference("table5").strip().splitlines()[1:]
+    assert len(t5) == 17 and sum(r.endswith(",half") for r in t5) == 7  # "7 out of 16" (PAPER.md:246)
