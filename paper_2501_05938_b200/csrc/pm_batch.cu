@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <tuple>
 
 #include "pm_batch.h"
@@ -285,7 +286,7 @@ cudaError_t launch_m(const BatchArgs& a0, const BatchPlan& pl, cudaStream_t st) 
   a.ntiles = pl.ntiles;
   auto kern = batch_cluster_kernel<M>;
   const size_t smem = batch_warp_bytes(M, pl.stages) * pl.warps + batch_cta_bytes(pl.kmax);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr(kern, smem);
   if (e != cudaSuccess) return e;
   if (pl.cluster > 8) {  // clusters of 9-16 CTAs are a B200 opt-in
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -310,15 +311,18 @@ cudaError_t launch_m(const BatchArgs& a0, const BatchPlan& pl, cudaStream_t st) 
 
 template <int M>
 int max_clusters(int cluster, int warps, int stages, int kmax) {
-  static std::map<std::tuple<int, int, int, int>, int> cache;
-  const auto key = std::make_tuple(cluster, warps, stages, kmax);
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int>, int> cache;  // + device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, cluster, warps, stages, kmax);
+  std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   auto kern = batch_cluster_kernel<M>;
   const size_t smem = batch_warp_bytes(M, stages) * warps + batch_cta_bytes(kmax);
   int n = 0;
-  if (smem <= 227 * 1024 &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+  if (smem <= 227 * 1024 && ensure_smem_attr(kern, smem) == cudaSuccess &&
       (cluster <= 8 ||
        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)) {
     cudaLaunchConfig_t cfg = {};

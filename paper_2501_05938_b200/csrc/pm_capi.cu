@@ -1323,6 +1323,9 @@ int pm_dist_set_peers(pm_handle_t h, void* const* peer_bufs, int32_t world, int3
   for (int k = 0; k < world; ++k)
     if (!peer_bufs[k]) return fail(h, PM_ERR_VALIDATION, "null peer buffer");
   PM_CUDA(h, cudaSetDevice(h->device));
+  // a new session: forget the previous epochs (callers barrier after this on
+  // every rank before the first pm_dist_reduce_p2p)
+  PM_CUDA(h, cudaMemset(h->xbuf, 0, exchange_bytes(world)));
   if (h->d_peers) PM_CUDA(h, cudaFree(h->d_peers));
   PM_CUDA(h, cudaMalloc(&h->d_peers, sizeof(void*) * world));
   PM_CUDA(h, cudaMemcpy(h->d_peers, peer_bufs, sizeof(void*) * world, cudaMemcpyHostToDevice));

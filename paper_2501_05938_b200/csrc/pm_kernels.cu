@@ -826,11 +826,9 @@ static cudaError_t launch_pair_one(const TileArgs& args, int warps_per_cta, int 
                                    cudaStream_t st, int* grid_out) {
   auto kern = warp_pair_kernel<M, MODE>;
   const size_t smem = pair_smem_bytes(M) * warps_per_cta;
-  static thread_local size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensure_smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, smem);
@@ -868,12 +866,9 @@ static cudaError_t launch_warp_one(const TileArgs& args, int warps_per_cta, int 
   auto kern = warp_tile_kernel<M, MODE, CHAIN>;
   const int m = (M > 0 ? M : args.m);
   const size_t smem = warp_smem_bytes(MODE, m, args.stages) * warps_per_cta;
-  static thread_local size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  {
+    cudaError_t e = ensure_smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta,
@@ -919,7 +914,7 @@ int warp_kernel_ctas_per_sm(int mode, int m, int stages, int warps_per_cta, bool
   const size_t smem = warp_smem_bytes(mode, m, stages) * warps_per_cta;
   int per_sm = 0;
   auto q = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem_attr(kern, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, smem);
   };
   const int M = m_is_specialised(m) ? m : 0;
@@ -1130,12 +1125,9 @@ static cudaError_t launch_one(const TileArgs& args, int P, int sm_count, cudaStr
   auto kern = tile_kernel<M, MODE, BULK>;
   const int S = BULK ? args.stages : 1;
   const size_t smem = tile_smem_bytes(MODE, P, (M > 0 ? M : args.m), S);
-  static thread_local size_t configured = 0;  // per-instantiation attribute cache
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  {
+    cudaError_t e = ensure_smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P, smem);

@@ -8,6 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "pm_device.cuh"
 
@@ -402,6 +405,25 @@ __device__ __forceinline__ void warp_downsweep(real& xf, real& xl, const Node* n
 #pragma unroll
   for (int k = 4; k >= 0; --k)
     down_level(nodes + warp_node_off(k), 1 << k, lane, 32, lane + (1 << k) < nblk, xf, xl);
+}
+
+// Raises a kernel's dynamic shared-memory limit once per (kernel, device):
+// cudaFuncSetAttribute applies to the current device only, so a per-thread
+// or per-process flag would miss the second GPU of a multi-device process.
+template <class K>
+inline cudaError_t ensure_smem_attr(K kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> configured;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = configured.find(key);
+  if (it != configured.end() && it->second >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) configured[key] = smem;
+  return e;
 }
 
 }  // namespace PM_NS

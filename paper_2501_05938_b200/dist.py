@@ -95,6 +95,8 @@ class DistributedSolver:
                 self._opened.append(p)
                 ptrs.append(p)
         self.solver.dist_set_peers(ptrs, self.rank)
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)  # every buffer cleared before anyone publishes
         # self-test: one exchange of tiny systems through the mapping
         dt = torch.float64
         n = 40
