@@ -81,6 +81,35 @@ def test_full_size_n8e7(solver):
     _check(xh, ah, bh, ch, dh)
 
 
+def _device_residual(a, b, c, d, x):
+    """||Ax - d||_2 / ||d||_2 in FP64 on the device (a[0], c[n-1] ignored)."""
+    r = b * x - d
+    r[1:] += a[1:] * x[:-1]
+    r[:-1] += c[:-1] * x[1:]
+    return float(r.norm() / d.norm())
+
+
+@pytest.mark.parametrize("n", [1_000_000_000, 1_000_000_007])
+def test_config5_size_on_one_gpu(solver, n):
+    """BASELINE config 5's system size N = 1e9 (40 GB of inputs) on one B200:
+    64-bit row indexing through every level (level 0: 3.1e6 warp tiles),
+    checked by the size-independent residual bar (FP64 on the device) and
+    by the FP64 generator's known structure; plus a second solve must be
+    bit-identical (deterministic kernels)."""
+    import torch
+
+    a, b, c, d = _device_system(solver, n, seed=5)
+    x = solver.solve_device(a, b, c, d, m=10)
+    solver.check()
+    res = _device_residual(a, b, c, d, x)
+    assert res <= RES_TOL, f"residual {res:.3e}"
+    x2 = solver.solve_device(a, b, c, d, m=10)
+    solver.check()
+    assert torch.equal(x, x2)
+    del a, b, c, d, x, x2
+    torch.cuda.empty_cache()
+
+
 def test_misaligned_pointers_use_fallback_path(solver):
     import torch
 
