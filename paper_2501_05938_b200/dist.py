@@ -15,7 +15,7 @@ last interface row is a real row, not padding).
 """
 from __future__ import annotations
 
-from .errors import ValidationError
+from .errors import CudaRuntimeError, ValidationError
 
 
 def split_rows(n: int, world: int, m: int) -> list[int]:
@@ -64,21 +64,37 @@ class DistributedSolver:
         self._opened = []
         self.exchange = "collective"
         if exchange in ("auto", "p2p"):
-            try:
-                self._setup_p2p()
+            if self._setup_p2p():
                 self.exchange = "p2p"
-            except Exception:
-                if exchange == "p2p":
-                    raise
+            elif exchange == "p2p":
+                raise CudaRuntimeError("P2P interface exchange unavailable on this group")
 
-    def _setup_p2p(self):
-        """Map every rank's exchange buffer (CUDA IPC) and register them."""
+    def _agree(self, ok: bool) -> bool:
+        """All ranks agree on a flag (logical AND over the group)."""
+        import torch
+
+        dev = self.iface.device if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(t.item())
+
+    def _setup_p2p(self) -> bool:
+        """Map every rank's exchange buffer (CUDA IPC) and register them, then
+        validate the mapping with one exchange.  Every rank takes part in the
+        same collectives whatever fails locally, and all ranks agree on the
+        outcome, so a partial failure falls back to the all-gather everywhere
+        instead of deadlocking."""
         import torch
 
         from .solver import ipc_get_handle, ipc_open_handle
 
-        own = self.solver.dist_exchange_alloc(self.world)
-        h = torch.frombuffer(bytearray(ipc_get_handle(own)), dtype=torch.uint8)
+        ok = True
+        try:
+            own = self.solver.dist_exchange_alloc(self.world)
+            raw = ipc_get_handle(own)
+        except Exception:
+            ok, own, raw = False, 0, bytes(64)
+        h = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
         if self.dist.get_backend(self.group) == "nccl":
             hs = [torch.empty(64, dtype=torch.uint8, device=self.iface.device) for _ in range(self.world)]
             self.dist.all_gather(hs, h.to(self.iface.device), group=self.group)
@@ -86,26 +102,38 @@ class DistributedSolver:
         else:
             hs = [torch.empty(64, dtype=torch.uint8) for _ in range(self.world)]
             self.dist.all_gather(hs, h, group=self.group)
-        ptrs = []
-        for k, hk in enumerate(hs):
-            if k == self.rank:
-                ptrs.append(own)
-            else:
-                p = ipc_open_handle(bytes(hk.numpy().tobytes()))
-                self._opened.append(p)
-                ptrs.append(p)
-        self.solver.dist_set_peers(ptrs, self.rank)
-        torch.cuda.synchronize()
-        self.dist.barrier(group=self.group)  # every buffer cleared before anyone publishes
-        # self-test: one exchange of tiny systems through the mapping
-        dt = torch.float64
-        n = 40
-        t = [torch.full((n,), v, dtype=dt, device=self.iface.device) for v in (0.5, 4.0, 0.5, 1.0)]
-        x = torch.empty(n, dtype=dt, device=self.iface.device)
-        self.solver.dist_reduce_p2p(*t, m=10)
-        self.solver.dist_solve_p2p(*t, x, m=10)
-        self.solver.check()
-        self.dist.barrier(group=self.group)
+        if ok:
+            try:
+                ptrs = []
+                for k, hk in enumerate(hs):
+                    if k == self.rank:
+                        ptrs.append(own)
+                    else:
+                        p = ipc_open_handle(bytes(hk.numpy().tobytes()))
+                        self._opened.append(p)
+                        ptrs.append(p)
+                self.solver.dist_set_peers(ptrs, self.rank)
+                torch.cuda.synchronize()
+            except Exception:
+                ok = False
+        # every buffer cleared (set_peers) before anyone publishes
+        if not self._agree(ok):
+            self.close()
+            return False
+        try:  # self-test: one exchange of tiny systems through the mapping
+            n = 40
+            t = [torch.full((n,), v, dtype=torch.float64, device=self.iface.device)
+                 for v in (0.5, 4.0, 0.5, 1.0)]
+            x = torch.empty(n, dtype=torch.float64, device=self.iface.device)
+            self.solver.dist_reduce_p2p(*t, m=10)
+            self.solver.dist_solve_p2p(*t, x, m=10)
+            self.solver.check()
+        except Exception:
+            ok = False
+        if not self._agree(ok):
+            self.close()
+            return False
+        return True
 
     def _all_gather(self):
         if self.iface.is_cuda and self.dist.get_backend(self.group) != "nccl":

@@ -77,7 +77,7 @@ class NumpyDistBackend:
         x[:] = torch.from_numpy(self._interior(aa, bb, cc, dd, xi[2 * rank], xi[2 * rank + 1]))
 
 
-def _worker(rank, world, port, n, m, q):
+def _worker(rank, world, port, n, m, q, exchange="collective"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -87,7 +87,10 @@ def _worker(rank, world, port, n, m, q):
         rows = split_rows(n, world, m)
         off = row_offset(n, world, m, rank)
         a, b, c, d = (torch.from_numpy(v[off:off + rows[rank]].copy()) for v in oracle.generate(n, 5))
-        ds = DistributedSolver(NumpyDistBackend(), device=torch.device("cpu"), exchange="collective")
+        ds = DistributedSolver(NumpyDistBackend(), device=torch.device("cpu"), exchange=exchange)
+        # "auto": the peer-memory setup cannot succeed without CUDA; every rank
+        # still joins the same collectives and all agree on the all-gather
+        assert ds.exchange == "collective"
         x = torch.empty(rows[rank], dtype=torch.float64)
         ds.solve(a, b, c, d, x, m=m)
         mx = max(rows)
@@ -103,12 +106,13 @@ def _worker(rank, world, port, n, m, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("exchange", ["collective", "auto"])
 @pytest.mark.parametrize("n,m,world", [(200, 10, 2), (157, 7, 2), (64, 4, 3)])
-def test_row_sharded_protocol_gloo(n, m, world):
+def test_row_sharded_protocol_gloo(n, m, world, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, m, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, m, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
