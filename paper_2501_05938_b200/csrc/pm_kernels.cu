@@ -345,6 +345,11 @@ __host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages) {
 #ifndef PM_SOLVE_MINB
 #define PM_SOLVE_MINB 4
 #endif
+// Stage 3 (level-0 warp tiles, rows in the stage): store x with one bulk
+// async copy per tile instead of the lanes' 16-byte stores
+#ifndef PM_X_BULK_STORE
+#define PM_X_BULK_STORE 1
+#endif
 #ifndef PM_REDUCE_MINB
 #define PM_REDUCE_MINB 1
 #endif
@@ -637,10 +642,32 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
         block_interior<0>(sacc, m, xf, xl, bad);
         for (int j = 0; j < m; ++j) bad |= !isfinite(sacc.x(j));
       }
-      __syncwarp();
-      // coalesced store of the tile's x
       real* gx = args.x + ctx.row0;
       const int v = ctx.valid;
+#if PM_X_BULK_STORE
+      if (kStageRows && (reinterpret_cast<uintptr_t>(gx) & 15) == 0 && ctx.bulk_rows > 0) {
+        // x leaves through one bulk store (TMA path) issued by lane 0; the
+        // stage is refilled once the store has read it
+        fence_proxy_async();  // this lane's x writes -> visible to the async proxy
+        __syncwarp();
+        if (lane == 0) {
+          bulk_s2g(gx, xsrc, static_cast<uint32_t>(ctx.bulk_rows * sizeof(real)));
+          bulk_commit();
+        }
+        for (int i = ctx.bulk_rows + lane; i < v; i += 32) gx[i] = xsrc[i];
+        __syncwarp();
+        if (k + S < nlocal) {
+          const int64_t tn = next_issue_tile(k + S);
+          if (lane == 0) {
+            bulk_wait_read0();
+            issue(s, tn);
+          }
+        }
+        continue;
+      }
+#endif
+      __syncwarp();
+      // coalesced store of the tile's x
       if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & (sizeof(real2) - 1)) == 0)) {
         const real2* s2 = reinterpret_cast<const real2*>(xsrc);
         real2* g2 = reinterpret_cast<real2*>(gx);
@@ -657,6 +684,9 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       }
     }
   }
+#if PM_X_BULK_STORE
+  if (MODE != kModeReduce && lane == 0) bulk_wait0();  // x stores complete before exit
+#endif
   if (bad) atomicOr(args.flag, 1);
 }
 
@@ -804,9 +834,26 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
           sb[r0 + M + j] = xv1[j];
         }
       }
-      __syncwarp();
       real* gx = args.x + ctx.row0;
       const int v = ctx.valid;
+#if PM_X_BULK_STORE
+      if ((reinterpret_cast<uintptr_t>(gx) & 15) == 0 && ctx.bulk_rows > 0) {
+        fence_proxy_async();  // x in the stage -> visible to the bulk store
+        __syncwarp();
+        if (lane == 0) {
+          bulk_s2g(gx, sb, static_cast<uint32_t>(ctx.bulk_rows * sizeof(real)));
+          bulk_commit();
+        }
+        for (int i = ctx.bulk_rows + lane; i < v; i += 32) gx[i] = sb[i];
+        __syncwarp();
+        if (lane == 0 && k + 1 < nlocal) {
+          bulk_wait_read0();
+          issue(tile_of(k + 1));
+        }
+        continue;
+      }
+#endif
+      __syncwarp();
       if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & (sizeof(real2) - 1)) == 0)) {
         const real2* s2 = reinterpret_cast<const real2*>(sb);
         real2* g2 = reinterpret_cast<real2*>(gx);
@@ -818,6 +865,9 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
       if (lane == 0 && k + 1 < nlocal) issue(tile_of(k + 1));
     }
   }
+#if PM_X_BULK_STORE
+  if (MODE != kModeReduce && lane == 0) bulk_wait0();
+#endif
   if (bad) atomicOr(args.flag, 1);
 }
 
