@@ -177,6 +177,16 @@ def cpu_partition_baseline(n: int, m: int, seed: int, reps: int, warm: int = 1):
     return n / statistics.median(times), threads, times
 
 
+def cpu_thomas_baseline(n: int, seed: int):
+    """Sequential Thomas on one core (SURVEY.md §8d baseline 1), one solve."""
+    import oracle
+
+    a, b, c, d = oracle.generate(n, seed)
+    t0 = time.perf_counter()
+    oracle.thomas(a, b, c, d)
+    return n / (time.perf_counter() - t0)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -550,7 +560,9 @@ def main():
         ups, threads, times = cpu_partition_baseline(n_loc, m, args.seed, reps=3)
         cpu = {"value": ups, "unit": "unknowns/s", "cores": threads, "kind": "port",
                "sample": f"full N={n_loc} system, median of 3 after 1 warm-up; oracle partition "
-                         f"method, Stage 1/3 OpenMP, Stage 2 serial; CPU: {model} ({cores} cpus)"}
+                         f"method, Stage 1/3 OpenMP, Stage 2 serial; CPU: {model} ({cores} cpus)",
+               "thomas_1core": {"value": cpu_thomas_baseline(n_loc, args.seed), "unit": "unknowns/s",
+                                "cores": 1, "sample": f"one sequential Thomas solve of N={n_loc}"}}
 
     if rank == 0:
         clocks = clk.summary()
