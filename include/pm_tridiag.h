@@ -112,6 +112,10 @@ typedef struct pm_model_bundle {
 #define PM_OPT_BATCH_STAGES 18 /* force bulk-copy stages per warp, 1..2 (0 = plan) */
 #define PM_OPT_UPPER_CTA_M 20  /* rows per thread of the CTA-tile upper levels (8) */
 #define PM_OPT_UPPER_CTA_P 21  /* threads per CTA tile of the upper levels (128)   */
+#define PM_OPT_GRAPHS 22       /* 1: device-resident solves (pm_solve_device_*,
+                                  level-kernel batches) replay a cached CUDA graph
+                                  per (arrays, sizes, options); stream must not be
+                                  the legacy default stream (default 0)            */
 #define PM_OPT_PAIR_TILES 19   /* level-0 pair tiles (two m-blocks per lane, 64*m
                                   rows per warp tile; m in {2, 8, 10, 16}):
                                   -1 (default) = on for FP32, off for FP64; 0; 1  */

@@ -187,6 +187,23 @@ struct pm_handle_s {
   int xworld = 0, xrank = -1;
   uint64_t epoch = 0;
   void* iface_local = nullptr;
+  // CUDA graphs of device-resident solves (PM_OPT_GRAPHS): one executable
+  // graph per (precision, arrays, sizes, plan generation, scratch) key
+  int use_graphs = 0;
+  uint64_t plan_gen = 0;  // bumped by every pm_set_option
+  struct GraphEntry {
+    size_t esz;
+    const void* p[5];
+    int64_t n, nps;
+    int m;
+    uint64_t gen;
+    const void* scratch;
+    cudaGraphExec_t exec;
+    int launches;
+    uint64_t last_use;
+  };
+  std::vector<GraphEntry> graphs;
+  uint64_t graph_clock = 0;
   // per-launch CUDA-event timing (PM_OPT_KERNEL_TIMES)
   int ktimes = 0;
   std::vector<cudaEvent_t> kev;
@@ -558,6 +575,64 @@ int read_flag(pm_handle_t h, cudaStream_t st) {
 
 // ---- the solver entry points, one instantiation per precision -------------
 
+// Runs `enqueue` (which enqueues the solve on `st`) through a cached CUDA
+// graph when PM_OPT_GRAPHS is on: the first call with a key records the
+// launches with stream capture and instantiates them; later calls replay
+// one cudaGraphLaunch.  The plan (and its scratch) is built before, outside
+// the capture.  Kernel-time recording bypasses graphs.  A capture the driver
+// rejects falls back to direct launches.
+template <class F>
+int run_maybe_graph(pm_handle_t h, cudaStream_t st, size_t esz, const void* const* ptrs, int64_t n,
+                    int64_t nps, int m, F&& enqueue) {
+  if (!h->use_graphs || h->ktimes || st == nullptr) return enqueue();
+  for (auto& g : h->graphs) {
+    if (g.esz == esz && g.n == n && g.nps == nps && g.m == m && g.gen == h->plan_gen &&
+        g.scratch == h->scratch && std::equal(ptrs, ptrs + 5, g.p)) {
+      g.last_use = ++h->graph_clock;
+      h->launches = g.launches;
+      PM_CUDA(h, cudaGraphLaunch(g.exec, st));
+      return PM_OK;
+    }
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return enqueue();
+  PM_CUDA(h, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int r = enqueue();
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(st, &graph);
+  if (r != PM_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return r;
+  }
+  cudaGraphExec_t exec = nullptr;
+  if (ee != cudaSuccess || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return enqueue();  // direct launches
+  }
+  cudaGraphDestroy(graph);
+  if (h->graphs.size() >= 8) {  // evict the least recently used
+    auto lru = std::min_element(h->graphs.begin(), h->graphs.end(),
+                                [](const auto& x, const auto& y) { return x.last_use < y.last_use; });
+    cudaGraphExecDestroy(lru->exec);
+    h->graphs.erase(lru);
+  }
+  pm_handle_s::GraphEntry g{};
+  g.esz = esz;
+  std::copy(ptrs, ptrs + 5, g.p);
+  g.n = n;
+  g.nps = nps;
+  g.m = m;
+  g.gen = h->plan_gen;
+  g.scratch = h->scratch;
+  g.exec = exec;
+  g.launches = h->launches;
+  g.last_use = ++h->graph_clock;
+  h->graphs.push_back(g);
+  PM_CUDA(h, cudaGraphLaunch(exec, st));
+  return PM_OK;
+}
+
 template <class R>
 int solve_device_impl(pm_handle_t h, const R* a, const R* b, const R* c,
                         const R* d, R* x, int64_t n, int32_t m, void* stream) {
@@ -568,7 +643,8 @@ int solve_device_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   if ((r = build_plan<R>(h, n, m, a, b, c, d, x, false, 0))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
-  return enq_full<R>(h, st, 0);
+  const void* ptrs[5] = {a, b, c, d, x};
+  return run_maybe_graph(h, st, sizeof(R), ptrs, n, 0, m, [&] { return enq_full<R>(h, st, 0); });
 }
 
 template <class R>
@@ -612,7 +688,9 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   }
   h->last_batch_plan = pm::BatchPlan{0, 0, 0, 0, 0, 0};
   if ((r = build_plan<R>(h, n, m, a, b, c, d, x, false, 0))) return r;
-  return enq_full<R>(h, st, batch > 1 ? n_per_system : 0);
+  const void* ptrs[5] = {a, b, c, d, x};
+  return run_maybe_graph(h, st, sizeof(R), ptrs, n, n_per_system, m,
+                         [&] { return enq_full<R>(h, st, batch > 1 ? n_per_system : 0); });
 }
 
 template <class R>
@@ -1041,6 +1119,7 @@ int pm_destroy(pm_handle_t h) {
   if (h->xbuf) cudaFree(h->xbuf);
   if (h->d_peers) cudaFree(h->d_peers);
   if (h->iface_local) cudaFree(h->iface_local);
+  for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   delete h;
   return PM_OK;
 }
@@ -1049,7 +1128,11 @@ const char* pm_last_error(pm_handle_t h) { return h ? h->err.c_str() : "null han
 
 int pm_set_option(pm_handle_t h, int option, int64_t value) {
   if (!h) return PM_ERR_VALIDATION;
+  ++h->plan_gen;  // recorded graphs of earlier settings are not reused
   switch (option) {
+    case PM_OPT_GRAPHS:
+      h->use_graphs = value ? 1 : 0;
+      return PM_OK;
     case PM_OPT_STAGES:
       if (value < 1 || value > 4) return fail(h, PM_ERR_VALIDATION, "stages must lie in [1, 4]");
       h->stages = (int)value;

@@ -38,6 +38,7 @@ PM_OPT_BATCH_STAGES = 18
 PM_OPT_PAIR_TILES = 19
 PM_OPT_UPPER_CTA_M = 20
 PM_OPT_UPPER_CTA_P = 21
+PM_OPT_GRAPHS = 22
 PM_MAX_M = 128
 
 

@@ -692,3 +692,46 @@ def test_pair_tiles_f32(pair_solver):
     a64[0] = 0.0
     c64[-1] = 0.0
     assert oracle.rel_err(x, oracle.thomas(a64, b64, c64, d64)) <= 1e-5
+
+
+def test_cuda_graph_replay(solver):
+    """PM_OPT_GRAPHS: record once, replay; new arrays / options record anew."""
+    import torch
+
+    from paper_2501_05938_b200.solver import PM_OPT_GRAPHS, PM_OPT_STAGES
+
+    st = torch.cuda.Stream()
+    solver.set_option(PM_OPT_GRAPHS, 1)
+    try:
+        for n, m in ((1_000_003, 10), (777, 10), (54_321, 7)):
+            a, b, c, d = _device_system(solver, n, seed=n % 13)
+            ref = [t.cpu().numpy() for t in (a, b, c, d)]
+            xs = []
+            for _ in range(3):  # record + 2 replays
+                with torch.cuda.stream(st):
+                    xs.append(solver.solve_device(a, b, c, d, m=m, stream=st))
+                solver.check()
+            for x in xs:
+                _check(x.cpu().numpy(), *ref)
+            # different inputs through the same arrays: the replay reads them anew
+            with torch.cuda.stream(st):
+                d.mul_(-2.0)
+                x = solver.solve_device(a, b, c, d, m=m, out=xs[0], stream=st)
+            solver.check()
+            _check(x.cpu().numpy(), ref[0], ref[1], ref[2], -2.0 * ref[3])
+        solver.set_option(PM_OPT_STAGES, 2)  # an option change records a new graph
+        a, b, c, d = _device_system(solver, 100_000, seed=3)
+        with torch.cuda.stream(st):
+            x = solver.solve_device(a, b, c, d, m=10, stream=st)
+            x2 = solver.solve_batch_device(a, b, c, d, n_per_system=10_000, m=10, stream=st)
+        solver.check()
+        _check(x.cpu().numpy(), *(t.cpu().numpy() for t in (a, b, c, d)))
+        ah, bh, ch, dh = (t.cpu().numpy() for t in (a, b, c, d))
+        for k in range(10):
+            sl = slice(k * 10_000, (k + 1) * 10_000)
+            sa, sc = ah[sl].copy(), ch[sl].copy()
+            sa[0] = 0.0
+            sc[-1] = 0.0
+            _check(x2.cpu().numpy()[sl], sa, bh[sl].copy(), sc, dh[sl].copy())
+    finally:
+        solver.set_option(PM_OPT_GRAPHS, 0)
