@@ -49,7 +49,9 @@ def _compile(src: Path) -> Path:
     rel = src.relative_to(CSRC)
     obj = BUILD / (str(rel).replace("/", "__") + ".o")
     obj.parent.mkdir(parents=True, exist_ok=True)
-    newest_dep = max([src.stat().st_mtime] + [h.stat().st_mtime for h in headers()])
+    # every object depends on every source and header: pm_kernels_f32.cu
+    # #includes pm_kernels.cu, so a per-file check would miss its edits
+    newest_dep = max([p.stat().st_mtime for p in sources()] + [h.stat().st_mtime for h in headers()])
     if obj.exists() and obj.stat().st_mtime >= newest_dep:
         return obj
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", *EXTRA,

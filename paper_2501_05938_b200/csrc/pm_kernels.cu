@@ -836,23 +836,6 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
       }
       real* gx = args.x + ctx.row0;
       const int v = ctx.valid;
-#if PM_X_BULK_STORE
-      if ((reinterpret_cast<uintptr_t>(gx) & 15) == 0 && ctx.bulk_rows > 0) {
-        fence_proxy_async();  // x in the stage -> visible to the bulk store
-        __syncwarp();
-        if (lane == 0) {
-          bulk_s2g(gx, sb, static_cast<uint32_t>(ctx.bulk_rows * sizeof(real)));
-          bulk_commit();
-        }
-        for (int i = ctx.bulk_rows + lane; i < v; i += 32) gx[i] = sb[i];
-        __syncwarp();
-        if (lane == 0 && k + 1 < nlocal) {
-          bulk_wait_read0();
-          issue(tile_of(k + 1));
-        }
-        continue;
-      }
-#endif
       __syncwarp();
       if ((v & 1) == 0 && ((reinterpret_cast<uintptr_t>(gx) & (sizeof(real2) - 1)) == 0)) {
         const real2* s2 = reinterpret_cast<const real2*>(sb);
@@ -865,9 +848,6 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
       if (lane == 0 && k + 1 < nlocal) issue(tile_of(k + 1));
     }
   }
-#if PM_X_BULK_STORE
-  if (MODE != kModeReduce && lane == 0) bulk_wait0();
-#endif
   if (bad) atomicOr(args.flag, 1);
 }
 
