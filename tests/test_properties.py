@@ -36,9 +36,12 @@ def test_total_is_additive_and_bounds_the_overlap_sum(vals, k, delta):
 def test_lower_bound_decreases_in_n(vals, ovh):
     t = timings(vals)
     prev = math.inf
+    s = st.overlap_sum(t)
+    rest = st.total_unstreamed(t) - s + ovh
     for n in (1, 2, 4, 8, 16, 32):
         lb = st.streamed_lower_bound(t, n, ovh)
-        if st.overlap_sum(t) > 0:
+        assert lb <= prev
+        if s > 1e-9 * (rest + 1.0):  # strictly, when the 1/n term is representable
             assert lb < prev
         prev = lb
     assert st.streamed_lower_bound(t, 1, 0.0) == pytest.approx(st.total_unstreamed(t), rel=1e-12)
