@@ -116,6 +116,7 @@ typedef struct pm_model_bundle {
                                   level-kernel batches) replay a cached CUDA graph
                                   per (arrays, sizes, options); stream must not be
                                   the legacy default stream (default 0)            */
+#define PM_OPT_PAIR_STAGES 23  /* bulk-copy ring depth of the pair-tile Stage 1 (1) */
 #define PM_OPT_PAIR_TILES 19   /* level-0 pair tiles (two m-blocks per lane, 64*m
                                   rows per warp tile; m in {2, 8, 10, 16}):
                                   -1 (default) = on for FP32, off for FP64; 0; 1  */

@@ -83,7 +83,7 @@ struct Prec<double> {
   static cudaError_t pair(int mode, const Args& a, int w, int sm, cudaStream_t st, int* g) {
     return pm::launch_warp_pair_kernel(mode, a, w, sm, st, g);
   }
-  static size_t pair_smem(int m) { return pm::pair_smem_bytes(m); }
+  static size_t pair_smem(int m, int S) { return pm::pair_smem_bytes(m, S); }
   static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st,
                                 const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
     return pm::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
@@ -115,7 +115,7 @@ struct Prec<float> {
   static cudaError_t pair(int mode, const Args& a, int w, int sm, cudaStream_t st, int* g) {
     return pm32::launch_warp_pair_kernel(mode, a, w, sm, st, g);
   }
-  static size_t pair_smem(int m) { return pm32::pair_smem_bytes(m); }
+  static size_t pair_smem(int m, int S) { return pm32::pair_smem_bytes(m, S); }
   static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st,
                                 const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
     return pm32::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
@@ -146,6 +146,7 @@ struct pm_handle_s {
   int solve_stages = 1;   // level-0 Stage 3 ring depth (0 = same as `stages`)
   int warps_per_cta = 4;
   int pair_tiles = -1;  // PM_OPT_PAIR_TILES: -1 auto (FP32 on, FP64 off)
+  int pair_stages = 1;  // PM_OPT_PAIR_STAGES: ring depth of the pair-tile Stage 1
   // batch cluster kernel
   int batch_cluster = 0;
   int batch_l2_mb = 64;
@@ -296,11 +297,13 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
   // chain mode, whose chunks are cut in 32-block tiles)
   const bool want_pair = h->pair_tiles > 0 || (h->pair_tiles < 0 && sizeof(R) == 4);
   if (L0.warps_per_cta > 0 && want_pair && pm::m_is_specialised(m) && !(h->opt_chain && allow_chain)) {
-    const int W = (int)std::min<size_t>(2, kSmemLimit / Prec<R>::pair_smem(m));
+    // Stage 1 rings h->pair_stages stages per warp, Stage 3 one (solve_stages)
+    const int S = std::max(1, std::min(h->pair_stages, 4));
+    const int W = (int)std::min<size_t>(2, kSmemLimit / Prec<R>::pair_smem(m, S));
     if (W >= 1) {
       L0.pair = true;
       L0.P = 64;
-      L0.stages = 1;
+      L0.stages = S;
       L0.warps_per_cta = W;
     }
   }
@@ -1206,6 +1209,10 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       if (value != 64 && value != 128 && value != 256)
         return fail(h, PM_ERR_VALIDATION, "upper CTA threads must be 64, 128 or 256");
       h->upper_cta_p = (int)value;
+      return PM_OK;
+    case PM_OPT_PAIR_STAGES:
+      if (value < 1 || value > 4) return fail(h, PM_ERR_VALIDATION, "pair stages must lie in [1, 4]");
+      h->pair_stages = (int)value;
       return PM_OK;
     case PM_OPT_PAIR_TILES:
       if (value < -1 || value > 1) return fail(h, PM_ERR_VALIDATION, "pair tiles is -1 (auto), 0 or 1");

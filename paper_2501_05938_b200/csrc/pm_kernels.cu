@@ -700,9 +700,10 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
 // pairs); Stage 1 releases it after the two block sweeps, Stage 3 after the
 // coalesced x store.  Same TileArgs, same level plan (P = 64 blocks per tile).
 // ---------------------------------------------------------------------------
-__host__ __device__ size_t pair_smem_bytes(int m) {
+__host__ __device__ size_t pair_smem_bytes(int m, int stages) {
   const size_t T = (size_t)64 * m;
-  const size_t bytes = 4 * T * sizeof(real) + 31 * sizeof(Node) + 2 * kMaxStages * sizeof(uint64_t);
+  const size_t bytes = (size_t)stages * 4 * T * sizeof(real) + 31 * sizeof(Node) +
+                       2 * kMaxStages * sizeof(uint64_t);
   return (bytes + 127) / 128 * 128;
 }
 
@@ -717,14 +718,12 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
   const int lane = threadIdx.x & 31;
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int r0 = lane * 2 * M;  // this lane's two blocks: rows [r0, r0 + M), [r0 + M, r0 + 2M)
-  const size_t per_warp = pair_smem_bytes(M);
+  const int S = args.stages;     // ring depth (Stage 1 may prefetch; Stage 3 uses 1)
+  const size_t per_warp = pair_smem_bytes(M, S);
   unsigned char* base = smem_raw + per_warp * warp;
-  real* sa = reinterpret_cast<real*>(base);
-  real* sb = sa + T;
-  real* sc = sb + T;
-  real* sd = sc + T;
-  Node* nodes = reinterpret_cast<Node*>(sd + T);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(base + per_warp - 2 * kMaxStages * sizeof(uint64_t));
+  real* stage0 = reinterpret_cast<real*>(base);
+  Node* nodes = reinterpret_cast<Node*>(stage0 + (size_t)S * 4 * T);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + per_warp - 2 * kMaxStages * sizeof(uint64_t));
 
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   const int64_t nwarp_total = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -734,27 +733,29 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     const int64_t idx = gwarp + k * nwarp_total;
     return args.reverse ? (args.tile_end - 1 - idx) : (args.tile_begin + idx);
   };
-  auto issue = [&](int64_t t) {
+  auto stage_ptr = [&](int st, int q) -> real* { return stage0 + ((size_t)st * 4 + q) * T; };
+  auto issue = [&](int st, int64_t t) {
     const int64_t row0 = t * T;
     const int64_t v = (args.n - row0 < T) ? (args.n - row0) : T;
     const uint32_t bytes = static_cast<uint32_t>((v & ~int64_t(kBulkRows - 1)) * sizeof(real));
     fence_proxy_async();
-    mbar_arrive_expect_tx(bar, 4u * bytes);
+    mbar_arrive_expect_tx(&bars[st], 4u * bytes);
     if (bytes) {
-      bulk_g2s(sa, args.a + row0, bytes, bar);
-      bulk_g2s(sb, args.b + row0, bytes, bar);
-      bulk_g2s(sc, args.c + row0, bytes, bar);
-      bulk_g2s(sd, args.d + row0, bytes, bar);
+      bulk_g2s(stage_ptr(st, 0), args.a + row0, bytes, &bars[st]);
+      bulk_g2s(stage_ptr(st, 1), args.b + row0, bytes, &bars[st]);
+      bulk_g2s(stage_ptr(st, 2), args.c + row0, bytes, &bars[st]);
+      bulk_g2s(stage_ptr(st, 3), args.d + row0, bytes, &bars[st]);
     }
   };
   if (lane == 0) {
-    mbar_init(bar, 1);
+    for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
     fence_mbar_init();
   }
   __syncwarp();
   pdl_launch_dependents();
   pdl_wait();
-  if (lane == 0 && nlocal > 0) issue(tile_of(0));
+  if (lane == 0)
+    for (int st = 0; st < S && st < nlocal; ++st) issue(st, tile_of(st));
 
   bool bad = false;
   real xf_next = 0.0, xl_next = 0.0;
@@ -784,7 +785,12 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     const int nblocks = args.pad_mode ? 64 : (ctx.valid + M - 1) / M;
     const int nlanes = (nblocks + 1) / 2;
     const bool has2 = 2 * lane + 1 < nblocks;
-    mbar_wait(bar, static_cast<uint32_t>(k & 1));
+    const int sidx = static_cast<int>(k % S);
+    real* sa = stage_ptr(sidx, 0);
+    real* sb = stage_ptr(sidx, 1);
+    real* sc = stage_ptr(sidx, 2);
+    real* sd = stage_ptr(sidx, 3);
+    mbar_wait(&bars[sidx], static_cast<uint32_t>((k / S) & 1));
 
     SmemAcc acc0{sa + r0, sb + r0, sc + r0, sd + r0, nullptr};
     SmemAcc acc1{sa + r0 + M, sb + r0 + M, sc + r0 + M, sd + r0 + M, nullptr};
@@ -799,7 +805,7 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     if (has2) combine(s0, s1, seg, lnode, bad);
     if constexpr (MODE == kModeReduce) {
       __syncwarp();
-      if (lane == 0 && k + 1 < nlocal) issue(tile_of(k + 1));  // stage released
+      if (lane == 0 && k + S < nlocal) issue(sidx, tile_of(k + S));  // stage released
       const Seg top = warp_upsweep(seg, nullptr, lane, nlanes, bad);
       if (lane == 0) {
         args.ra[2 * t] = top.F.a; args.rb[2 * t] = top.F.b;
@@ -845,7 +851,7 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
         for (int i = lane; i < v; i += 32) gx[i] = sb[i];
       }
       __syncwarp();
-      if (lane == 0 && k + 1 < nlocal) issue(tile_of(k + 1));
+      if (lane == 0 && k + S < nlocal) issue(sidx, tile_of(k + S));
     }
   }
   if (bad) atomicOr(args.flag, 1);
@@ -855,7 +861,7 @@ template <int M, int MODE>
 static cudaError_t launch_pair_one(const TileArgs& args, int warps_per_cta, int sm_count,
                                    cudaStream_t st, int* grid_out) {
   auto kern = warp_pair_kernel<M, MODE>;
-  const size_t smem = pair_smem_bytes(M) * warps_per_cta;
+  const size_t smem = pair_smem_bytes(M, args.stages) * warps_per_cta;
   {
     cudaError_t e = ensure_smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
