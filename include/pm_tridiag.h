@@ -220,11 +220,13 @@ int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const dou
  * side channel (e.g. torch.distributed), maps them with pm_ipc_open_handle
  * and calls pm_dist_set_peers with every rank's buffer in rank order (its
  * own included).  Then per solve, on every rank:
- *   pm_dist_reduce_p2p_*  Stage 1 + local levels, then one kernel stores the
- *                         rank's 8 interface reals into every peer's buffer
- *                         and releases an epoch flag (system scope);
- *   pm_dist_solve_p2p_*   one thread acquires all ranks' flags, solves the
- *                         2*world-row interface system, then Stage 3.
+ *   pm_dist_reduce_p2p_*  Stage 1 + local levels; the top-level kernel that
+ *                         produces the rank's 8 interface reals stores them
+ *                         into every peer's buffer and releases an epoch
+ *                         flag (system scope) itself;
+ *   pm_dist_solve_p2p_*   the top-level Stage-3 kernel acquires all ranks'
+ *                         flags, solves the 2*world-row interface system,
+ *                         then every level's Stage 3 (at most 64 ranks).
  * No host synchronisation or collective call on the data path.  A peer that
  * never publishes makes the wait time out after 20 s (PM_ERR_RUNTIME from
  * pm_check).  Ranks must call the pair in lockstep (collective semantics). */

@@ -84,13 +84,8 @@ struct Prec<double> {
     return pm::launch_warp_pair_kernel(mode, a, w, sm, st, g);
   }
   static size_t pair_smem(int m, int S) { return pm::pair_smem_bytes(m, S); }
-  static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st,
-                                const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
-    return pm::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
-  }
-  static cudaError_t publish(const double* iface, void* const* peers, int w, int r, uint64_t e,
-                             cudaStream_t st) {
-    return pm::launch_dist_publish(iface, peers, w, r, e, st);
+  static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st) {
+    return pm::launch_dist_chain(ia, w, r, xb, f, st);
   }
   static cudaError_t generate(double* a, double* b, double* c, double* d, int64_t n, int64_t r0,
                               int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
@@ -116,13 +111,8 @@ struct Prec<float> {
     return pm32::launch_warp_pair_kernel(mode, a, w, sm, st, g);
   }
   static size_t pair_smem(int m, int S) { return pm32::pair_smem_bytes(m, S); }
-  static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st,
-                                const uint64_t* flags = nullptr, uint64_t epoch = 0, uint64_t tmo = 0) {
-    return pm32::launch_dist_chain(ia, w, r, xb, f, st, flags, epoch, tmo);
-  }
-  static cudaError_t publish(const float* iface, void* const* peers, int w, int r, uint64_t e,
-                             cudaStream_t st) {
-    return pm32::launch_dist_publish(iface, peers, w, r, e, st);
+  static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st) {
+    return pm32::launch_dist_chain(ia, w, r, xb, f, st);
   }
   static cudaError_t generate(float* a, float* b, float* c, float* d, int64_t n, int64_t r0,
                               int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
@@ -188,6 +178,12 @@ struct pm_handle_s {
   int xworld = 0, xrank = -1;
   uint64_t epoch = 0;
   void* iface_local = nullptr;
+  // set while a pm_dist_*_p2p call enqueues its top level: that launch
+  // publishes (REDUCE) or acquires and chains (SOLVE) the interface rows itself
+  struct P2PTop {
+    bool active = false;
+    uint64_t epoch = 0;
+  } p2p_top;
   // CUDA graphs of device-resident solves (PM_OPT_GRAPHS): one executable
   // graph per (precision, arrays, sizes, plan generation, scratch) key
   int use_graphs = 0;
@@ -462,6 +458,16 @@ void set_chain(pm_handle_t h, typename Prec<R>::Args& A, int part) {
 }
 
 template <class R>
+void set_p2p(pm_handle_t h, typename Prec<R>::Args& A) {
+  A.xpeers = h->d_peers;
+  A.xlocal = h->xbuf;
+  A.xworld = h->xworld;
+  A.xrank = h->xrank;
+  A.xepoch = h->p2p_top.epoch;
+  A.xtimeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s
+}
+
+template <class R>
 int enq_reduce(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, bool zf, bool zl,
                int64_t sys_len, R* const* out4, int part = 0) {
   const Level& L = h->levels[k];
@@ -477,6 +483,7 @@ int enq_reduce(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st,
   A.zero_last = zl;
   A.sys_len = (k == 0) ? sys_len : 0;
   if (k == 0 && h->chain) set_chain<R>(h, A, part);
+  if (h->p2p_top.active && k + 1 == h->levels.size()) set_p2p<R>(h, A);
   return launch<R>(h, pm::kModeReduce, A, L, st);
 }
 
@@ -492,6 +499,7 @@ int enq_solve(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, 
   A.sys_len = (k == 0) ? sys_len : 0;
   A.reverse = h->reverse;
   if (k == 0 && h->chain) set_chain<R>(h, A, part);
+  if (h->p2p_top.active && k + 1 == h->levels.size()) set_p2p<R>(h, A);
   return launch<R>(h, pm::kModeSolve, A, L, st);
 }
 
@@ -931,12 +939,19 @@ int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
   R* xb = reinterpret_cast<R*>(h->scratch);  // extra_elems region
-  PM_CUDA(h, Prec<R>::dist_chain(iface_all, world, rank, xb, h->dflag, st, flags, epoch,
-                                  20ull * 1000 * 1000 * 1000 /* 20 s */));
-  ++h->launches;
   const bool zf = rank == 0, zl = last;
   const size_t top = h->levels.size() - 1;
-  if ((r = enq_solve<R>(h, top, 0, 1, st, zf, zl, 0, xb))) return r;
+  if (flags) {  // P2P: the top-level SOLVE acquires and chains the interface rows itself
+    h->p2p_top.active = true;
+    h->p2p_top.epoch = epoch;
+    r = enq_solve<R>(h, top, 0, 1, st, zf, zl, 0, xb);
+    h->p2p_top.active = false;
+    if (r) return r;
+  } else {
+    PM_CUDA(h, Prec<R>::dist_chain(iface_all, world, rank, xb, h->dflag, st));
+    ++h->launches;
+    if ((r = enq_solve<R>(h, top, 0, 1, st, zf, zl, 0, xb))) return r;
+  }
   for (size_t k = top; k-- > 0;)
     if ((r = enq_solve<R>(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
   return PM_OK;
@@ -1064,13 +1079,14 @@ int dist_reduce_p2p_impl(pm_handle_t h, const R* a, const R* b, const R* c, cons
   if (!h) return PM_ERR_VALIDATION;
   if (!h->d_peers || h->xworld < 1) return fail(h, PM_ERR_VALIDATION, "pm_dist_set_peers not called");
   if (!h->iface_local) PM_CUDA(h, cudaMalloc(&h->iface_local, 8 * sizeof(double)));
-  int r = dist_reduce_impl<R>(h, a, b, c, d, n_local, m, h->xrank, h->xworld,
-                              static_cast<R*>(h->iface_local), stream);
+  // the rank's top-level REDUCE publishes its two rows to every peer itself
+  h->p2p_top.active = true;
+  h->p2p_top.epoch = h->epoch + 1;
+  const int r = dist_reduce_impl<R>(h, a, b, c, d, n_local, m, h->xrank, h->xworld,
+                                    static_cast<R*>(h->iface_local), stream);
+  h->p2p_top.active = false;
   if (r) return r;
   ++h->epoch;
-  PM_CUDA(h, Prec<R>::publish(static_cast<const R*>(h->iface_local), h->d_peers, h->xworld, h->xrank,
-                              h->epoch, static_cast<cudaStream_t>(stream)));
-  ++h->launches;
   return PM_OK;
 }
 
@@ -1408,6 +1424,7 @@ int pm_dist_exchange_alloc(pm_handle_t h, int32_t world, void** out) {
 int pm_dist_set_peers(pm_handle_t h, void* const* peer_bufs, int32_t world, int32_t rank) {
   if (!h || !peer_bufs) return PM_ERR_VALIDATION;
   if (world < 1 || rank < 0 || rank >= world) return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  if (world > 64) return fail(h, PM_ERR_VALIDATION, "the P2P exchange supports at most 64 ranks");
   if (!h->xbuf || h->xbuf_world != world)
     return fail(h, PM_ERR_VALIDATION, "pm_dist_exchange_alloc(world) must precede pm_dist_set_peers");
   for (int k = 0; k < world; ++k)

@@ -136,6 +136,97 @@ __device__ __forceinline__ void cta_downsweep(real& xf, real& xl, TreeSmem& tr,
 }
 
 // ---------------------------------------------------------------------------
+// Peer-memory exchange (NVLink P2P) of the interface equations, replacing the
+// all-gather.  Every rank owns an exchange buffer laid out as
+//   [2 parities][world][8] reals  |  [2 parities][world] uint64 epochs
+// (pm_dist_exchange_bytes).  The rank's top-level REDUCE (p2p_publish) stores
+// its 8 reals into slot [epoch & 1][r] of every peer's buffer, then a
+// system-scope fence and a release store of the epoch into the peer's flag
+// [epoch & 1][r]; the top-level SOLVE (p2p_chain) spins on acquire loads of
+// its own flags until every rank's epoch arrived, then chains the rows.  Two
+// parities: a rank can run ahead by one solve only (its next publish needs
+// every peer's current publish).  No separate exchange kernel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int kMaxP2PWorld = 64;
+
+// Thread 0 of a rank's top-level REDUCE: publish the rank's two interface rows
+// (layout per rank [Fa, La, Fb, Lb, Fc, Lc, Fd, Ld]) into every peer.
+__device__ void p2p_publish(const Seg& top, const TileArgs& A) {
+  const real v[8] = {top.F.a, top.L.a, top.F.b, top.L.b, top.F.c, top.L.c, top.F.d, top.L.d};
+  const int par = static_cast<int>(A.xepoch & 1);
+  for (int k = 0; k < A.xworld; ++k) {
+    real* dst = static_cast<real*>(A.xpeers[k]) + ((size_t)par * A.xworld + A.xrank) * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[j] = v[j];
+  }
+  __threadfence_system();
+  for (int k = 0; k < A.xworld; ++k) {
+    uint64_t* flags =
+        reinterpret_cast<uint64_t*>(static_cast<real*>(A.xpeers[k]) + (size_t)2 * A.xworld * 8);
+    st_release_sys(flags + par * A.xworld + A.xrank, A.xepoch);
+  }
+}
+
+// Thread 0 of a rank's top-level SOLVE: wait for every rank's rows, chain the
+// 2*world-row interface system, solve its 2x2, walk back to this rank.
+// Returns false on a timeout (flag bit 4).
+__device__ bool p2p_chain(const TileArgs& A, real& xf, real& xl, bool& bad) {
+  const int W = A.xworld, par = static_cast<int>(A.xepoch & 1);
+  const real* iface = static_cast<const real*>(A.xlocal) + (size_t)par * W * 8;
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(static_cast<const real*>(A.xlocal) +
+                                                            (size_t)2 * W * 8);
+  const uint64_t t0 = global_ns();
+  for (int k = 0; k < W; ++k) {
+    while (ld_acquire_sys(flags + par * W + k) < A.xepoch) {
+      if (global_ns() - t0 > A.xtimeout_ns) {
+        atomicOr(A.flag, 4);
+        return false;
+      }
+      __nanosleep(256);
+    }
+  }
+  auto seg_of = [&](int k) {
+    const real* p = iface + 8 * k;
+    return Seg{Row{p[0], p[2], p[4], p[6]}, Row{p[1], p[3], p[5], p[7]}};
+  };
+  Node cn[kMaxP2PWorld];
+  Seg acc = seg_of(0);
+  for (int k = 1; k < W; ++k) combine(acc, seg_of(k), acc, cn[k], bad);
+  const real det = fma(acc.F.b, acc.L.b, -acc.F.c * acc.L.a);
+  bad |= (det == 0.0);
+  const real inv = drcp(det);
+  const real x0 = fma(acc.F.d, acc.L.b, -acc.F.c * acc.L.d) * inv;
+  real xr = fma(acc.F.b, acc.L.d, -acc.L.a * acc.F.d) * inv;
+  real xfr = x0;
+  for (int k = W - 1; k >= 1 && k >= A.xrank; --k) {
+    real xl_prev, xf_k;
+    split_node(cn[k], x0, xr, xl_prev, xf_k);
+    if (k == A.xrank) {
+      xfr = xf_k;
+      break;
+    }
+    xr = xl_prev;
+  }
+  xf = xfr;
+  xl = xr;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // The tile kernel
 // ---------------------------------------------------------------------------
 template <int M, int MODE, bool BULK>
@@ -249,7 +340,9 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     Seg top = cta_upsweep(seg, tree, MODE == kModeReduce ? nullptr : wnodes, lane, warp, nwarps,
                           nblk, bad);
     if constexpr (MODE == kModeReduce) {
-      if (tid == 0) {
+      if (tid == 0 && args.xpeers) {
+        p2p_publish(top, args);
+      } else if (tid == 0) {
         args.ra[2 * t] = top.F.a; args.rb[2 * t] = top.F.b;
         args.rc[2 * t] = top.F.c; args.rd[2 * t] = top.F.d;
         args.ra[2 * t + 1] = top.L.a; args.rb[2 * t + 1] = top.L.b;
@@ -265,6 +358,8 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
           const real inv = drcp(det);
           xf = fma(top.F.d, top.L.b, -top.F.c * top.L.d) * inv;
           xl = fma(top.F.b, top.L.d, -top.L.a * top.F.d) * inv;
+        } else if (args.xworld > 0) {
+          p2p_chain(args, xf, xl, bad);
         } else {
           xf = args.xb[2 * t];
           xl = args.xb[2 * t + 1];
@@ -981,69 +1076,12 @@ int warp_kernel_ctas_per_sm(int mode, int m, int stages, int warps_per_cta, bool
 // final 2x2 (rank 0's F.a and rank world-1's L.c are zero), then walk the
 // chain back down to this rank.
 // ---------------------------------------------------------------------------
-// Peer-memory exchange (NVLink P2P) of the interface equations, replacing
-// the all-gather.  Every rank owns an exchange buffer laid out as
-//   [2 parities][world][8] reals  |  [2 parities][world] uint64 epochs
-// (pm_dist_exchange_bytes).  Publish: rank r stores its 8 reals into slot
-// [epoch & 1][r] of every peer's buffer, then a system-scope fence and a
-// release store of the epoch into the peer's flag [epoch & 1][r].  The solve
-// side (dist_chain_kernel with flags) spins on acquire loads of its own flags
-// until every rank's epoch arrived.  Two parities: a rank can run ahead by
-// one solve only (its next publish needs every peer's current publish).
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t global_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-__global__ void dist_publish_kernel(const real* __restrict__ iface, void* const* __restrict__ peers,
-                                    int world, int rank, uint64_t epoch) {
-  const int k = threadIdx.x;  // destination rank
-  if (k >= world) return;
-  const int par = static_cast<int>(epoch & 1);
-  real* slots = static_cast<real*>(peers[k]);
-  uint64_t* flags = reinterpret_cast<uint64_t*>(slots + (size_t)2 * world * 8);
-  real* dst = slots + ((size_t)par * world + rank) * 8;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) dst[j] = iface[j];
-  __threadfence_system();
-  st_release_sys(flags + par * world + rank, epoch);
-}
-
-cudaError_t launch_dist_publish(const real* iface, void* const* peers, int world, int rank,
-                                uint64_t epoch, cudaStream_t st) {
-  dist_publish_kernel<<<1, ((world + 31) / 32) * 32, 0, st>>>(iface, peers, world, rank, epoch);
-  return cudaGetLastError();
-}
-
+// (all-gather path; the P2P path chains inside the top-level SOLVE, p2p_chain)
 __global__ void dist_chain_kernel(const real* __restrict__ iface, int world, int rank,
-                                  real* __restrict__ xb, int* flag, const uint64_t* flags,
-                                  uint64_t epoch, uint64_t timeout_ns) {
+                                  real* __restrict__ xb, int* flag) {
   extern __shared__ Node chain_nodes[];
   if (threadIdx.x != 0) return;
   bool bad = false;
-  if (flags) {  // P2P exchange: wait for every rank's interface equations
-    const int par = static_cast<int>(epoch & 1);
-    const uint64_t t0 = global_ns();
-    for (int k = 0; k < world; ++k) {
-      while (ld_acquire_sys(flags + par * world + k) < epoch) {
-        if (global_ns() - t0 > timeout_ns) {  // a peer never published
-          atomicOr(flag, 4);
-          return;
-        }
-        __nanosleep(256);
-      }
-    }
-    iface += (size_t)par * world * 8;
-  }
   // per rank: [Fa, La, Fb, Lb, Fc, Lc, Fd, Ld] (the REDUCE kernel's output
   // layout for a one-tile level: ra = p, rb = p + 2, rc = p + 4, rd = p + 6)
   auto seg_of = [&](int k) {
@@ -1077,11 +1115,10 @@ __global__ void dist_chain_kernel(const real* __restrict__ iface, int world, int
 }
 
 cudaError_t launch_dist_chain(const real* iface_all, int world, int rank, real* xb, int* flag,
-                              cudaStream_t st, const uint64_t* flags, uint64_t epoch,
-                              uint64_t timeout_ns) {
+                              cudaStream_t st) {
   const size_t smem = (size_t)world * sizeof(Node);
   if (smem > 48 * 1024) return cudaErrorInvalidValue;
-  dist_chain_kernel<<<1, 32, smem, st>>>(iface_all, world, rank, xb, flag, flags, epoch, timeout_ns);
+  dist_chain_kernel<<<1, 32, smem, st>>>(iface_all, world, rank, xb, flag);
   return cudaGetLastError();
 }
 
