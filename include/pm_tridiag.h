@@ -159,7 +159,12 @@ int pm_solve_batch_host_f32(pm_handle_t h, const float* a, const float* b, const
                             int32_t depth, int64_t systems_per_chunk);
 
 /* Waits for the handle's last stream; PM_ERR_COMPUTATION if any solve since
- * the previous check met a zero or non-finite pivot (the flag is cleared). */
+ * the previous check met a zero or non-finite pivot (the flag is cleared).
+ * After a flagged device-resident solve (pm_solve_device_*, pm_solve_batch_
+ * device_*; x not aliasing an input) pm_check first re-runs that solve once
+ * with classic pivot sweeps -- the fast continuant pivots can leave the FP
+ * range for rows scaled over >~1e60 -- and reports only if that fails too;
+ * so the inputs must be unchanged until pm_check. */
 int pm_check(pm_handle_t h);
 
 /* End-to-end solve from host memory (synchronous).  num_streams in

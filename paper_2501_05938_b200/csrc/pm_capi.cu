@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
@@ -201,6 +202,11 @@ struct pm_handle_s {
   };
   std::vector<GraphEntry> graphs;
   uint64_t graph_clock = 0;
+  // pivot-failure retry: a solve whose fast (continuant) pivots leave the
+  // FP range for extremely scaled rows is re-run once with classic sweeps
+  int robust_mode = 0;
+  std::function<int()> retry;  // re-enqueues the last device-resident solve
+  cudaStream_t retry_stream = nullptr;
   // per-launch CUDA-event timing (PM_OPT_KERNEL_TIMES)
   int ktimes = 0;
   std::vector<cudaEvent_t> kev;
@@ -291,7 +297,7 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
   }
   // pair tiles: two m-blocks per lane, 64*m rows per warp tile (not with
   // chain mode, whose chunks are cut in 32-block tiles)
-  const bool want_pair = h->pair_tiles > 0 || (h->pair_tiles < 0 && sizeof(R) == 4);
+  const bool want_pair = !h->robust_mode && (h->pair_tiles > 0 || (h->pair_tiles < 0 && sizeof(R) == 4));
   if (L0.warps_per_cta > 0 && want_pair && pm::m_is_specialised(m) && !(h->opt_chain && allow_chain)) {
     // Stage 1 rings h->pair_stages stages per warp, Stage 3 one (solve_stages)
     const int S = std::max(1, std::min(h->pair_stages, 4));
@@ -412,6 +418,7 @@ typename Prec<R>::Args args_for(pm_handle_t h, const Level& L, int64_t t0, int64
   A.max_ctas = h->max_ctas;
   A.flag = h->dflag;
   A.pad_mode = L.pad_mode;
+  A.robust = h->robust_mode;
   return A;
 }
 
@@ -573,6 +580,21 @@ int read_flag(pm_handle_t h, cudaStream_t st) {
   int flag = 0;
   PM_CUDA(h, cudaMemcpyAsync(&flag, h->dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
   PM_CUDA(h, cudaStreamSynchronize(st));
+  if (flag == 1 && h->retry && !h->robust_mode) {
+    // a zero / non-finite pivot in the fast path: redo the last solve with
+    // classic sweeps (continuant products can leave the FP range for rows
+    // scaled over many orders of magnitude); report only if that fails too
+    PM_CUDA(h, cudaMemsetAsync(h->dflag, 0, sizeof(int), st));
+    PM_CUDA(h, cudaStreamSynchronize(st));
+    h->robust_mode = 1;
+    const int r = h->retry();
+    h->robust_mode = 0;
+    cudaStream_t rs = h->retry_stream;
+    if (r) return r;
+    PM_CUDA(h, cudaStreamSynchronize(rs));
+    PM_CUDA(h, cudaMemcpyAsync(&flag, h->dflag, sizeof(int), cudaMemcpyDeviceToHost, rs));
+    PM_CUDA(h, cudaStreamSynchronize(rs));
+  }
   if (flag) {
     PM_CUDA(h, cudaMemsetAsync(h->dflag, 0, sizeof(int), st));
     PM_CUDA(h, cudaStreamSynchronize(st));
@@ -595,7 +617,7 @@ int read_flag(pm_handle_t h, cudaStream_t st) {
 template <class F>
 int run_maybe_graph(pm_handle_t h, cudaStream_t st, size_t esz, const void* const* ptrs, int64_t n,
                     int64_t nps, int m, F&& enqueue) {
-  if (!h->use_graphs || h->ktimes || st == nullptr) return enqueue();
+  if (!h->use_graphs || h->ktimes || h->robust_mode || st == nullptr) return enqueue();
   for (auto& g : h->graphs) {
     if (g.esz == esz && g.n == n && g.nps == nps && g.m == m && g.gen == h->plan_gen &&
         g.scratch == h->scratch && std::equal(ptrs, ptrs + 5, g.p)) {
@@ -655,6 +677,14 @@ int solve_device_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
   const void* ptrs[5] = {a, b, c, d, x};
+  h->retry = nullptr;  // (x aliasing an input: the inputs are gone, no retry)
+  if (x != a && x != b && x != c && x != d) {
+    h->retry = [h, a, b, c, d, x, n, m, st]() {
+      int rr = build_plan<R>(h, n, m, a, b, c, d, x, false, 0);
+      return rr ? rr : enq_full<R>(h, st, 0);
+    };
+    h->retry_stream = st;
+  }
   return run_maybe_graph(h, st, sizeof(R), ptrs, n, 0, m, [&] { return enq_full<R>(h, st, 0); });
 }
 
@@ -672,8 +702,17 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   h->launches = 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
+  if (!h->robust_mode) {
+    h->retry = nullptr;
+    if (x != a && x != b && x != c && x != d) {
+      h->retry = [h, a, b, c, d, x, n_per_system, batch, m, stream]() {
+        return solve_batch_impl<R>(h, a, b, c, d, x, n_per_system, batch, m, stream);
+      };
+      h->retry_stream = st;
+    }
+  }
   pm::BatchPlan pl{};
-  if (std::is_same<R, double>::value && batch > 1 && h->batch_cluster && aligned16(a) && aligned16(b) && aligned16(c) &&
+  if (std::is_same<R, double>::value && batch > 1 && h->batch_cluster && !h->robust_mode && aligned16(a) && aligned16(b) && aligned16(c) &&
       aligned16(d) && aligned16(x) &&
       pm::plan_batch(m, n_per_system, batch, h->sm_count, (int64_t)h->batch_l2_mb << 20,
                      h->batch_force_cluster, h->batch_force_warps, h->batch_force_stages, &pl)) {
@@ -709,6 +748,7 @@ int solve_host_impl(pm_handle_t h, const R* a, const R* b, const R* c,
                       const R* d, R* x, int64_t n, int32_t m, int32_t num_streams) {
   int r = validate_common(h, a, b, c, d, x, n, m);
   if (r) return r;
+  h->retry = nullptr;
   if (num_streams != 0 && !streamtune::StreamCount::is_valid(num_streams))
     return fail(h, PM_ERR_VALIDATION,
                 streamtune::InvalidStreamCountError(num_streams).what());
@@ -875,6 +915,14 @@ int solve_host_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   }
   cleanup();
   h->last_stream = main;
+  // retry on the staged device copies (separate from x, so host aliasing is fine)
+  h->retry = [h, da, db, dc, dd, dx, x, n, m, main]() {
+    int rr = build_plan<R>(h, n, m, da, db, dc, dd, dx, false, 0);
+    if (!rr) rr = enq_full<R>(h, main, 0);
+    if (!rr) PM_CUDA(h, cudaMemcpyAsync(x, dx, (size_t)n * sizeof(R), cudaMemcpyDeviceToHost, main));
+    return rr;
+  };
+  h->retry_stream = main;
   return read_flag(h, main);
 }
 
@@ -896,6 +944,7 @@ template <class R>
 int dist_reduce_impl(pm_handle_t h, const R* a, const R* b, const R* c,
                        const R* d, int64_t n_local, int32_t m, int32_t rank, int32_t world,
                        R* iface, void* stream) {
+  if (h) h->retry = nullptr;  // collective: no single-rank retry
   // x is not used by the reduce; pass d so the plan's alignment test sees a real pointer
   int r = validate_common(h, a, b, c, d, d, n_local, m);
   if (r) return r;
@@ -924,6 +973,7 @@ int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
                       const R* d, R* x, int64_t n_local, int32_t m, int32_t rank,
                       int32_t world, const R* iface_all, void* stream,
                       const uint64_t* flags = nullptr, uint64_t epoch = 0) {
+  if (h) h->retry = nullptr;  // collective: no single-rank retry
   int r = validate_common(h, a, b, c, d, x, n_local, m);
   if (r) return r;
   if (!iface_all) return fail(h, PM_ERR_VALIDATION, "null iface_all pointer");
@@ -1060,6 +1110,7 @@ int solve_batch_host_impl(pm_handle_t h, const R* a, const R* b, const R* c, con
   cudaError_t se = cudaStreamSynchronize(s_out);
   if (se == cudaSuccess) se = cudaStreamSynchronize(s_comp);
   cleanup();
+  h->retry = nullptr;  // the per-chunk retries are gone with the staging slots
   if (se != cudaSuccess) return cuda_fail(h, se, "batch solve");
   h->launches = launches;
   h->last_stream = s_comp;

@@ -424,18 +424,18 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
 
 // Per-warp shared memory: [stages][a,b,c,d][T] | x buffer | 31 tree nodes | mbarriers.
 // The x buffer exists only for Stage 3 with rows in registers (runtime m).
-__host__ __device__ size_t warp_xbuf_doubles(int mode, int m) {
-  const bool stage_rows = PM_SOLVE_STAGE_ROWS != 0 && (m == 2 || m == 8 || m == 10 || m == 16);
+__host__ __device__ size_t warp_xbuf_doubles(int mode, int m, bool spec) {
+  // spec: the compile-time-m instantiation (keeps the rows in the stage)
+  const bool stage_rows = PM_SOLVE_STAGE_ROWS != 0 && spec && (m == 2 || m == 8 || m == 10 || m == 16);
   return (mode != kModeReduce && !stage_rows) ? (size_t)32 * m : 0;
 }
 
-__host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages) {
+__host__ __device__ size_t warp_smem_bytes(int mode, int m, int stages, bool spec) {
   const size_t T = (size_t)32 * m;
-  size_t bytes = (size_t)stages * 4 * T * sizeof(real) + warp_xbuf_doubles(mode, m) * sizeof(real) +
+  size_t bytes = (size_t)stages * 4 * T * sizeof(real) + warp_xbuf_doubles(mode, m, spec) * sizeof(real) +
                  31 * sizeof(Node) + 2 * kMaxStages * sizeof(uint64_t);
   return (bytes + 127) / 128 * 128;
 }
-
 
 #ifndef PM_SOLVE_MINB
 #define PM_SOLVE_MINB 4
@@ -476,11 +476,11 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int S = args.stages;
   const int r0 = lane * m;
-  const size_t per_warp = warp_smem_bytes(MODE, m, S);
+  const size_t per_warp = warp_smem_bytes(MODE, m, S, M > 0);
   unsigned char* base = smem_raw + per_warp * warp;
   real* stage0 = reinterpret_cast<real*>(base);
   real* xbuf = stage0 + (size_t)S * 4 * T;
-  Node* nodes = reinterpret_cast<Node*>(xbuf + warp_xbuf_doubles(MODE, m));
+  Node* nodes = reinterpret_cast<Node*>(xbuf + warp_xbuf_doubles(MODE, m, M > 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + per_warp - 2 * kMaxStages * sizeof(uint64_t));
 
   const int64_t gwarp = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
@@ -996,7 +996,7 @@ static cudaError_t launch_warp_one(const TileArgs& args, int warps_per_cta, int 
                                    cudaStream_t st, int* grid_out) {
   auto kern = warp_tile_kernel<M, MODE, CHAIN>;
   const int m = (M > 0 ? M : args.m);
-  const size_t smem = warp_smem_bytes(MODE, m, args.stages) * warps_per_cta;
+  const size_t smem = warp_smem_bytes(MODE, m, args.stages, M > 0) * warps_per_cta;
   {
     cudaError_t e = ensure_smem_attr(kern, smem);
     if (e != cudaSuccess) return e;
@@ -1025,7 +1025,8 @@ static cudaError_t launch_warp_m(int mode, const TileArgs& args, int warps_per_c
   return red ? launch_warp_one<MM, kModeReduce, CHAIN>(args, warps_per_cta, sm_count, st,      \
                                                         grid_out)                              \
              : launch_warp_one<MM, kModeSolve, CHAIN>(args, warps_per_cta, sm_count, st, grid_out)
-  switch (m_is_specialised(args.m) ? args.m : 0) {
+  // robust (retry) launches take the runtime-m kernels: classic sweeps only
+  switch (!args.robust && m_is_specialised(args.m) ? args.m : 0) {
     case 2: PM_WARP_CASE(2);
     case 8: PM_WARP_CASE(8);
     case 10: PM_WARP_CASE(10);
@@ -1042,7 +1043,7 @@ cudaError_t launch_warp_tile_kernel(int mode, const TileArgs& args, int warps_pe
 }
 
 int warp_kernel_ctas_per_sm(int mode, int m, int stages, int warps_per_cta, bool chain) {
-  const size_t smem = warp_smem_bytes(mode, m, stages) * warps_per_cta;
+  const size_t smem = warp_smem_bytes(mode, m, stages, m_is_specialised(m)) * warps_per_cta;
   int per_sm = 0;
   auto q = [&](auto kern) {
     ensure_smem_attr(kern, smem);
@@ -1231,7 +1232,7 @@ bool m_is_specialised(int m) { return m == 2 || m == 8 || m == 10 || m == 16; }
 
 cudaError_t launch_tile_kernel(int mode, const TileArgs& args, int P, bool bulk, int sm_count,
                                cudaStream_t st, int* grid_out) {
-  const int Mspec = m_is_specialised(args.m) ? args.m : 0;
+  const int Mspec = (!args.robust && m_is_specialised(args.m)) ? args.m : 0;  // robust: classic
   if (mode == kModeReduce)
     return bulk ? dispatch_m<kModeReduce, true>(Mspec, args, P, sm_count, st, grid_out)
                 : dispatch_m<kModeReduce, false>(Mspec, args, P, sm_count, st, grid_out);

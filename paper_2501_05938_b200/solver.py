@@ -218,7 +218,9 @@ class PartitionSolver:
         return x
 
     def check(self):
-        """pm_check: synchronise and raise ComputationError on a pivot failure."""
+        """pm_check: synchronise and raise ComputationError on a pivot failure.
+        After a flagged device-resident solve it first re-runs that solve with
+        classic pivot sweeps (into the same x), so read x after check()."""
         self._ok(self._L.pm_check(self._h))
 
     def generate_device(self, n: int, seed: int = 42, device=None, stream=None, arrays=None, dtype=None):

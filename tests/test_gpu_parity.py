@@ -735,3 +735,55 @@ def test_cuda_graph_replay(solver):
             _check(x2.cpu().numpy()[sl], sa, bh[sl].copy(), sc, dh[sl].copy())
     finally:
         solver.set_option(PM_OPT_GRAPHS, 0)
+
+
+@pytest.mark.parametrize("span", [0, 20, 70, 100, 150])
+def test_row_scaled_systems(solver, span):
+    """Rows scaled by random powers of ten (the solution is unchanged): exercises
+    the continuant range checks, the fast path's finiteness fallback to the
+    classic sweep and the power-of-two scaling inside `combine` across row
+    magnitudes 1e-span..1e+span.  Supported range: |log10 scale| <= 150 (the
+    reduced rows' products must stay inside FP64's exponent range)."""
+    import torch
+
+    n = 300_007
+    a, b, c, d = oracle.generate(n, 77)
+    rng = np.random.default_rng(span)
+    sc = 10.0 ** rng.uniform(-span, span, n)
+    a2, b2, c2, d2 = a * sc, b * sc, c * sc, d * sc
+    t = [torch.from_numpy(v.copy()).cuda() for v in (a2, b2, c2, d2)]
+    xr = oracle.thomas(a, b, c, d)  # same solution as the unscaled system
+    for m in (10, 7, 16, 2):
+        xd = solver.solve_device(*t, m=m)
+        solver.check()  # a flagged fast-pivot solve is re-run with classic sweeps into xd
+        x = xd.cpu().numpy()
+        assert oracle.rel_err(x, xr) <= REL_TOL
+        assert oracle.residual(a, b, c, d, x) <= RES_TOL
+    # the same through the host path and a batch of two copies
+    x = solver.solve_host(*(np.ascontiguousarray(v) for v in (a2, b2, c2, d2)), m=10)
+    assert oracle.rel_err(x, xr) <= REL_TOL
+    tb = [torch.cat([v, v]) for v in t]
+    xbd = solver.solve_batch_device(*tb, n_per_system=n, m=10)
+    solver.check()
+    xb = xbd.cpu().numpy()
+    assert oracle.rel_err(xb[:n], xr) <= REL_TOL and oracle.rel_err(xb[n:], xr) <= REL_TOL
+
+
+@pytest.mark.parametrize("span", [0, 5, 12])
+def test_row_scaled_systems_f32(solver, span):
+    import torch
+
+    n = 200_003
+    a, b, c, d = oracle.generate(n, 78)
+    rng = np.random.default_rng(span + 1)
+    sc = 10.0 ** rng.uniform(-span, span, n)
+    v32 = [(v * sc).astype(np.float32) for v in (a, b, c, d)]
+    t = [torch.from_numpy(v).cuda() for v in v32]
+    xd = solver.solve_device(*t, m=10)
+    solver.check()  # FP32: a flagged fast-pivot solve is re-run with classic sweeps
+    x = xd.cpu().numpy().astype(np.float64)
+    a64, b64, c64, d64 = (v.astype(np.float64) for v in v32)
+    a64[0] = 0.0
+    c64[-1] = 0.0
+    xr = oracle.thomas(a64, b64, c64, d64)
+    assert oracle.rel_err(x, xr) <= 1e-5
