@@ -9,9 +9,11 @@
 #include <vector>
 
 #include "pm_tridiag.h"
+#include "streamtune/bundle_io.hpp"
 #include "streamtune/dataset.hpp"
 #include "streamtune/errors.hpp"
 #include "streamtune/predictor.hpp"
+#include "streamtune/simulator.hpp"
 #include "streamtune/timing_model.hpp"
 
 int main(int argc, char** argv) {
@@ -36,6 +38,15 @@ int main(int argc, char** argv) {
   const Recommendation r = recommend(ModelBundle::paper(), 1000000);
   std::printf("paper bundle: N=1e6 -> %d streams; B200 bundle: N=8e7 -> %d streams\n",
               r.chosen.value(), recommend(ModelBundle::b200(), 80000000).chosen.value());
+  // --- simulator, model document, report harness ---------------
+  PipelineSpec p = PipelineSpec::from_timings(t, StreamCount(8), 0.004448);
+  const SimResult sr = simulate(p);
+  std::printf("simulated T_str(8) %.6f ms, Eq. 2 bound holds: %s\n", sr.total_ms,
+              verify_lower_bound(p) ? "yes" : "no");
+  const ModelBundle back = bundle_from_document(bundle_to_document(ModelBundle::b200()));
+  const TableReport t4 = report_table(ModelBundle::paper(), "table4");
+  std::printf("bundle round trip exact: %s; Table 4: %d PASS, %d FAIL, %d KNOWN\n",
+              back.sum_a == ModelBundle::b200().sum_a ? "yes" : "no", t4.passed, t4.failed, t4.known);
   // --- solver C ABI --------------------------------------------------------------
   if (argc > 1 && std::strcmp(argv[1], "--solve") == 0) {
     const int64_t n = 1000003;
@@ -64,6 +75,25 @@ int main(int argc, char** argv) {
     pm_last_stage_timings(h, &tm, &total, &used);
     std::printf("solved n=%lld with %d streams in %.3f ms, residual %.3e\n", (long long)n, used,
                 total, std::sqrt(res / nd));
+    // the FP32 twin and a batch of 3 copies from host memory
+    std::vector<float> a32(a.begin(), a.end()), b32(b.begin(), b.end()), c32(c.begin(), c.end()),
+        d32(d.begin(), d.end()), x32(n);
+    st = pm_solve_host_f32(h, a32.data(), b32.data(), c32.data(), d32.data(), x32.data(), n, 10, 0);
+    double err32 = 0.0, nx = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      err32 = std::fmax(err32, std::fabs(x32[i] - x[i]));
+      nx = std::fmax(nx, std::fabs(x[i]));
+    }
+    std::vector<double> ab, bb, cb, db, xb(3 * n);
+    for (int k = 0; k < 3; ++k) {
+      ab.insert(ab.end(), a.begin(), a.end()); bb.insert(bb.end(), b.begin(), b.end());
+      cb.insert(cb.end(), c.begin(), c.end()); db.insert(db.end(), d.begin(), d.end());
+    }
+    const int stb = pm_solve_batch_host_f64(h, ab.data(), bb.data(), cb.data(), db.data(), xb.data(), n,
+                                            3, 10, 0, 0);
+    double errb = 0.0;
+    for (int64_t i = 0; i < 3 * n; ++i) errb = std::fmax(errb, std::fabs(xb[i] - x[i % n]));
+    std::printf("fp32 status %d rel err %.2e; batch status %d max diff %.2e\n", st, err32 / nx, stb, errb);
     pm_destroy(h);
   }
   return 0;

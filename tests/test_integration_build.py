@@ -23,6 +23,8 @@ def test_cpp_caller_builds_and_runs(tmp_path):
     out = subprocess.run([str(_build(tmp_path))], check=True, capture_output=True, text=True).stdout
     assert "benefit(8) 1.415968" in out  # PAPER.md:156 (Table 2)
     assert "caught InvalidStreamCountError(3)" in out
+    assert "Eq. 2 bound holds: yes" in out
+    assert "bundle round trip exact: yes; Table 4: 24 PASS, 0 FAIL, 1 KNOWN" in out
 
 
 def test_c_header_is_plain_c(tmp_path):
@@ -41,3 +43,6 @@ def test_cpp_caller_solves_on_gpu(tmp_path):
     out = subprocess.run([str(_build(tmp_path)), "--solve"], check=True, capture_output=True, text=True).stdout
     line = [l for l in out.splitlines() if l.startswith("solved")][0]
     assert float(line.split("residual")[1]) < 1e-12
+    line = [l for l in out.splitlines() if l.startswith("fp32 status")][0].split()
+    assert line[2] == "0" and float(line[5].rstrip(";")) < 1e-5
+    assert line[8] == "0" and float(line[11]) < 1e-12
