@@ -787,3 +787,23 @@ def test_row_scaled_systems_f32(solver, span):
     c64[-1] = 0.0
     xr = oracle.thomas(a64, b64, c64, d64)
     assert oracle.rel_err(x, xr) <= 1e-5
+
+
+def test_bench_batch_sharded_path(tmp_path):
+    """bench.py --workload batch with two ranks sharing cuda:0 (gloo): the batch
+    splits over the ranks with no collective on the data path."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29677", str(root / "bench.py"),
+           "--gpus", "2", "--workload", "batch", "--batch", "9", "--batch-rows", "20000", "--steps", "3",
+           "--warmup", "3", "--e2e-steps", "2", "--dist-backend", "gloo", "--same-device"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["systems_per_gpu"] == [5, 4]
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["scaling"] == "strong"
