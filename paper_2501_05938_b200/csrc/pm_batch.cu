@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(512, 1) batch_cluster_kernel(BatchArgs args) {
     fence_mbar_init();
   }
   __syncwarp();
-  pdl_launch_dependents();
   pdl_wait();
+  pdl_launch_dependents();
   if (lane == 0)
     for (int s = 0; s < S && s < njobs; ++s) issue(s, s);
 

@@ -269,8 +269,9 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     }
   };
 
-  pdl_launch_dependents();
+  // dependents launch only after this kernel's own wait (see warp_tile_kernel)
   pdl_wait();
+  pdl_launch_dependents();
   if constexpr (BULK) {
     if (tid == 0) {
       for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -551,8 +552,15 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     fence_mbar_init();
   }
   __syncwarp();
+  // Programmatic dependent launch.  Every kernel of a solve lets its dependents
+  // launch only after its own griddepcontrol.wait, so once a Stage-3 launch
+  // exists, Stage 1 of the same solve has passed its wait: every earlier write
+  // to a, b, c, d is complete and visible.  Stage 3 therefore issues its first
+  // tiles' loads and runs their Stage-1 sweeps and trees before waiting; only
+  // the level above's x (xb) needs the wait, taken at the first downsweep.
+  constexpr bool kLateWait = (MODE != kModeReduce) && !CHAIN;
+  if constexpr (!kLateWait) pdl_wait();
   pdl_launch_dependents();
-  pdl_wait();
   for (int s = 0; s < S && s < nlocal; ++s) {
     const int64_t t = next_issue_tile(s);  // all lanes advance the cursor
     if (lane == 0) issue(s, t);
@@ -570,11 +578,7 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
   if (MODE != kModeReduce && nlocal > 0) {
     if constexpr (CHAIN) {
       if (lane == 0 && cc.hi - cc.lo > 1) nd_next = args.chain_nodes[cc.hi - 1];
-    } else {
-      const int64_t t0 = tile_of(0);
-      xf_next = __ldg(args.xb + 2 * t0);
-      xl_next = __ldg(args.xb + 2 * t0 + 1);
-    }
+    }  // strided mode: tile 0's values after the wait (kLateWait)
   }
   Seg acc;  // Stage 1 chain accumulator (lane 0)
   for (int64_t k = 0; k < nlocal; ++k) {
@@ -615,7 +619,7 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
             if (tn != cc.lo) nd_next = args.chain_nodes[tn];
           }
         }
-      } else if (k + 1 < nlocal) {
+      } else if (k > 0 && k + 1 < nlocal) {
         const int64_t tn = tile_of(k + 1);
         xf_next = __ldg(args.xb + 2 * tn);
         xl_next = __ldg(args.xb + 2 * tn + 1);
@@ -705,6 +709,18 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
       }
     } else {
       real xf = xf_tile, xl = xl_tile;
+      if constexpr (kLateWait) {
+        if (k == 0) {
+          pdl_wait();
+          xf = __ldg(args.xb + 2 * t);
+          xl = __ldg(args.xb + 2 * t + 1);
+          if (nlocal > 1) {
+            const int64_t tn = tile_of(1);
+            xf_next = __ldg(args.xb + 2 * tn);
+            xl_next = __ldg(args.xb + 2 * tn + 1);
+          }
+        }
+      }
       __syncwarp();  // nodes written by lanes are read by the same lanes only
       warp_downsweep(xf, xl, nodes, lane, nblk);
       const real* xsrc = kStageRows ? sb : xbuf;
@@ -847,8 +863,8 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     fence_mbar_init();
   }
   __syncwarp();
-  pdl_launch_dependents();
   pdl_wait();
+  pdl_launch_dependents();
   if (lane == 0)
     for (int st = 0; st < S && st < nlocal; ++st) issue(st, tile_of(st));
 
