@@ -269,8 +269,11 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     }
   };
 
-  // dependents launch only after this kernel's own wait (see warp_tile_kernel)
-  pdl_wait();
+  // Dependents launch only after this kernel's own wait (see warp_tile_kernel),
+  // except from a SOLVE: a SOLVE launch exists only once the ROOT passed its
+  // wait, i.e. every REDUCE of the solve completed, so its level's rows are
+  // final; it loads and reduces its first tile before waiting for xb.
+  if constexpr (MODE != kModeSolve) pdl_wait();
   pdl_launch_dependents();
   if constexpr (BULK) {
     if (tid == 0) {
@@ -351,6 +354,9 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
       }
     } else {
       real xf = 0.0, xl = 0.0;
+      if constexpr (MODE == kModeSolve) {
+        if (k == 0) pdl_wait();
+      }
       if (tid == 0) {
         if constexpr (MODE == kModeRoot) {
           // top.F.a and top.L.c multiply unknowns outside the system (zero).
