@@ -492,7 +492,7 @@ def main():
     t_solve, t_reduce = avg(1), avg(0)
     per_kernel = {}
     for (md, lv, t) in ktimes:
-        per_kernel.setdefault(f"{['reduce', 'solve', 'root', 'up_solve'][md]}_L{lv}", []).append(t)
+        per_kernel.setdefault(f"{['reduce', 'solve', 'root', 'upper', 'cluster'][md]}_L{lv}", []).append(t)
     per_kernel = {k: round(sum(v) / len(v), 5) for k, v in sorted(per_kernel.items())}
     t_kern_total = sum(t for (_, _, t) in ktimes) / args.steps
     peak, peak_src = peaks()

@@ -117,6 +117,11 @@ typedef struct pm_model_bundle {
                                   per (arrays, sizes, options); stream must not be
                                   the legacy default stream (default 0)            */
 #define PM_OPT_PAIR_STAGES 23  /* bulk-copy ring depth of the pair-tile Stage 1 (1) */
+#define PM_OPT_UPPER_FUSED 24  /* 1 (default): levels 1-2 of a three-level plan
+                                  (both of 128 x 8 CTA tiles, level 2 one tile)
+                                  in one launch, one co-resident CTA per level-1
+                                  tile: reduce, last CTA solves level 2, each
+                                  back-solves its tile (3 launches -> 1); 0: off */
 #define PM_OPT_PAIR_TILES 19   /* level-0 pair tiles (two m-blocks per lane, 64*m
                                   rows per warp tile; m in {2, 8, 10, 16}):
                                   -1 (default) = on for FP32, off for FP64; 0; 1  */
@@ -282,7 +287,8 @@ int pm_dist_solve_f32(pm_handle_t h, const float* a, const float* b, const float
 int pm_last_launch_count(pm_handle_t h);
 /* Per-launch durations (ms) recorded since the last call while
  * PM_OPT_KERNEL_TIMES is on; mode 0 = Stage-1 reduce, 1 = Stage-3 solve,
- * 2 = root; level 0 = the caller's system.  Synchronises; returns the count. */
+ * 2 = root, 3 = fused upper levels (recorded as level 1), 4 = batch cluster
+ * kernel; level 0 = the caller's system.  Synchronises; returns the count. */
 int pm_kernel_times(pm_handle_t h, int32_t* modes, int32_t* levels, float* ms, int32_t max);
 int pm_last_plan(pm_handle_t h, int64_t* rows_per_level, int32_t max_levels);
 

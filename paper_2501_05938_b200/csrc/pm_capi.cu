@@ -85,6 +85,11 @@ struct Prec<double> {
     return pm::launch_warp_pair_kernel(mode, a, w, sm, st, g);
   }
   static size_t pair_smem(int m, int S) { return pm::pair_smem_bytes(m, S); }
+  using UpperArgs = pm::UpperArgs;
+  static int upper_capacity(int sm) { return pm::upper_fused_capacity(sm); }
+  static cudaError_t upper(const UpperArgs& u, int sm, cudaStream_t st, int* g) {
+    return pm::launch_upper_fused(u, sm, st, g);
+  }
   static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st) {
     return pm::launch_dist_chain(ia, w, r, xb, f, st);
   }
@@ -112,6 +117,11 @@ struct Prec<float> {
     return pm32::launch_warp_pair_kernel(mode, a, w, sm, st, g);
   }
   static size_t pair_smem(int m, int S) { return pm32::pair_smem_bytes(m, S); }
+  using UpperArgs = pm32::UpperArgs;
+  static int upper_capacity(int sm) { return pm32::upper_fused_capacity(sm); }
+  static cudaError_t upper(const UpperArgs& u, int sm, cudaStream_t st, int* g) {
+    return pm32::launch_upper_fused(u, sm, st, g);
+  }
   static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st) {
     return pm32::launch_dist_chain(ia, w, r, xb, f, st);
   }
@@ -149,6 +159,9 @@ struct pm_handle_s {
   char* scratch = nullptr;  // level arrays of the current solve's precision
   size_t scratch_bytes = 0;
   int* dflag = nullptr;
+  unsigned long long* dsync = nullptr;  // counters of the fused upper-level kernel
+  int upper_fused = 1;                  // PM_OPT_UPPER_FUSED
+  int upper_cap[2] = {-1, -1};          // its co-resident CTAs (FP64, FP32; -1: not queried)
   // device staging for the host path: a, b, c, d, x
   char* hbuf = nullptr;
   size_t hbuf_bytes = 0;
@@ -519,12 +532,61 @@ int enq_root(pm_handle_t h, size_t k, cudaStream_t st, int64_t sys_len) {
 }
 
 
+// Levels 1-2 in one launch (pm::launch_upper_fused): a three-level plan with
+// levels 1 and 2 of 128 x 8 CTA tiles, level 2 a single tile, and every
+// level-1 tile's CTA co-resident.  Not in robust mode (classic sweeps).
+template <class R>
+bool upper_fusable(pm_handle_t h) {
+  if (!h->upper_fused || h->robust_mode || h->chain || h->p2p_top.active || h->levels.size() != 3)
+    return false;
+  auto cta8 = [](const Level& L) {
+    return L.warps_per_cta == 0 && !L.pair && L.P == pm::kUpperP && L.m == pm::kUpperM && L.pad_mode == 1;
+  };
+  const Level& L1 = h->levels[1];
+  const Level& L2 = h->levels[2];
+  if (!cta8(L1) || !cta8(L2) || L2.ntiles != 1 || L2.n != 2 * L1.ntiles) return false;
+  int& cap = h->upper_cap[sizeof(R) == 4];
+  if (cap < 0) cap = Prec<R>::upper_capacity(h->sm_count);
+  return L1.ntiles <= cap;
+}
+
+template <class R>
+int enq_upper_fused(pm_handle_t h, cudaStream_t st) {
+  const Level& L1 = h->levels[1];
+  const Level& L2 = h->levels[2];
+  typename Prec<R>::UpperArgs u;
+  u.a1 = static_cast<const R*>(L1.a); u.b1 = static_cast<const R*>(L1.b);
+  u.c1 = static_cast<const R*>(L1.c); u.d1 = static_cast<const R*>(L1.d);
+  u.x1 = static_cast<R*>(L1.x);
+  u.n1 = L1.n;
+  u.a2 = static_cast<R*>(const_cast<void*>(L2.a)); u.b2 = static_cast<R*>(const_cast<void*>(L2.b));
+  u.c2 = static_cast<R*>(const_cast<void*>(L2.c)); u.d2 = static_cast<R*>(const_cast<void*>(L2.d));
+  u.x2 = static_cast<R*>(L2.x);
+  u.n2 = L2.n;
+  u.sync = h->dsync;
+  u.flag = h->dflag;
+  const bool timed = h->ktimes && next_kevent(h) != nullptr;
+  const size_t ev = h->krec.size() * 2;
+  if (timed) cudaEventRecord(h->kev[ev], st);
+  int grid = 0;
+  const cudaError_t e = Prec<R>::upper(u, h->sm_count, st, &grid);
+  if (e != cudaSuccess) return cuda_fail(h, e, "fused upper-level kernel launch");
+  if (timed) {
+    cudaEventRecord(h->kev[ev + 1], st);
+    h->krec.push_back({3, 1, ev});
+  }
+  if (grid > 0) ++h->launches;
+  return PM_OK;
+}
+
 // Upper levels (1..top) on one stream: REDUCE 1..top-1, ROOT top, SOLVE
-// top-1..1 (chain mode: level 1 is the top, a single ROOT).
+// top-1..1 (chain mode: level 1 is the top, a single ROOT), or the fused
+// single launch when it applies.
 template <class R>
 int enq_upper(pm_handle_t h, cudaStream_t st) {
   const size_t top = h->levels.size() - 1;
   int r;
+  if (upper_fusable<R>(h)) return enq_upper_fused<R>(h, st);
   for (size_t k = 1; k < top; ++k)
     if ((r = enq_reduce<R>(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
   if (top >= 1 && (r = enq_root<R>(h, top, st, 0))) return r;
@@ -599,6 +661,10 @@ int read_flag(pm_handle_t h, cudaStream_t st) {
     PM_CUDA(h, cudaMemsetAsync(h->dflag, 0, sizeof(int), st));
     PM_CUDA(h, cudaStreamSynchronize(st));
     if (flag & 4) return fail(h, PM_ERR_RUNTIME, "P2P interface exchange timed out (a peer never published)");
+    if (flag & 8) {
+      PM_CUDA(h, cudaMemset(h->dsync, 0, 8 * sizeof(unsigned long long)));
+      return fail(h, PM_ERR_RUNTIME, "fused upper-level kernel: level-2 flag wait timed out");
+    }
     return fail(h, PM_ERR_COMPUTATION, "zero or non-finite pivot (system not solvable without pivoting)");
   }
   return PM_OK;
@@ -1167,6 +1233,8 @@ int pm_create(pm_handle_t* out, int device) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (e == cudaSuccess) e = cudaMalloc(&h->dflag, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(h->dflag, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&h->dsync, 8 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(h->dsync, 0, 8 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->main, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete h;
@@ -1186,6 +1254,7 @@ int pm_destroy(pm_handle_t h) {
   if (h->scratch) cudaFree(h->scratch);
   if (h->hbuf) cudaFree(h->hbuf);
   if (h->dflag) cudaFree(h->dflag);
+  if (h->dsync) cudaFree(h->dsync);
   if (h->xbuf) cudaFree(h->xbuf);
   if (h->d_peers) cudaFree(h->d_peers);
   if (h->iface_local) cudaFree(h->iface_local);
@@ -1276,6 +1345,9 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       if (value != 64 && value != 128 && value != 256)
         return fail(h, PM_ERR_VALIDATION, "upper CTA threads must be 64, 128 or 256");
       h->upper_cta_p = (int)value;
+      return PM_OK;
+    case PM_OPT_UPPER_FUSED:
+      h->upper_fused = value ? 1 : 0;
       return PM_OK;
     case PM_OPT_PAIR_STAGES:
       if (value < 1 || value > 4) return fail(h, PM_ERR_VALIDATION, "pair stages must lie in [1, 4]");

@@ -43,9 +43,9 @@ bool g_use_pdl = true;
 #endif
 
 // Launch with the programmatic-stream-serialization attribute (PDL).
-template <class K>
+template <class K, class A>
 static cudaError_t launch_kernel(K kern, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                                 const TileArgs& args) {
+                                 const A& args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -416,6 +416,208 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     if (tid == 0) bulk_wait0();
   }
   if (bad) atomicOr(args.flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Upper levels in one launch (PM_OPT_UPPER_FUSED): a plan whose level 1 is
+// CTA tiles (128 threads x 8 rows) and whose level 2 is a single such tile.
+// One CTA per level-1 tile, all co-resident: each reduces its tile (rows kept
+// in registers, tree nodes in shared memory) and publishes the tile's two rows
+// into level 2; the last CTA to finish (ticket) solves level 2 and releases a
+// flag; every CTA then back-solves its own tile from level 2's x.  Replaces
+// the REDUCE, ROOT and SOLVE launches and their two dependency hand-offs, and
+// level 1 is read once instead of twice.  Counters (sync[0..2]) start at zero
+// and every launch leaves them at zero; a flag wait longer than 1 s sets bit 8
+// of the status flag instead of hanging.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct UpperSmem {
+  real rows[4][kUpperP * kUpperM];      // this CTA's level-1 tile, kept to the end
+  Node wnodes[2][(kUpperP / 32) * 31];  // tree nodes: own tile | level 2 (last CTA)
+  TreeSmem tree[2];
+  int last;
+};
+
+size_t upper_smem_bytes() { return sizeof(UpperSmem); }
+
+__device__ __forceinline__ TileCtx upper_ctx(const real* ga, const real* gb, const real* gc, const real* gd,
+                                             int64_t n, int64_t t) {
+  constexpr int T = kUpperP * kUpperM;
+  TileCtx ctx;
+  ctx.ga = ga; ctx.gb = gb; ctx.gc = gc; ctx.gd = gd;
+  ctx.row0 = t * T;
+  ctx.n = n;
+  ctx.valid = static_cast<int>((n - ctx.row0 < T) ? (n - ctx.row0) : T);
+  ctx.bulk_rows = ctx.valid;  // every valid row comes from shared memory
+  ctx.zf = true;
+  ctx.zl = true;
+  ctx.sys_len = 0;
+  return ctx;
+}
+
+// Rows of one thread (8 consecutive rows of tile t) straight from global
+// memory (L2-resident level arrays); rows past n are identity rows.
+__device__ __forceinline__ void upper_regs_global(const real* ga, const real* gb, const real* gc,
+                                                  const real* gd, int64_t n, int64_t t,
+                                                  RegAcc<kUpperM>& r) {
+  const int64_t g0 = t * (kUpperP * kUpperM) + threadIdx.x * kUpperM;
+#pragma unroll
+  for (int j = 0; j < kUpperM; ++j) {
+    const int64_t g = g0 + j;
+    const bool in = g < n;
+    r.A[j] = (in && g > 0) ? __ldcg(ga + g) : real(0);
+    r.B[j] = in ? __ldcg(gb + g) : real(1);
+    r.C[j] = (in && g < n - 1) ? __ldcg(gc + g) : real(0);
+    r.D[j] = in ? __ldcg(gd + g) : real(0);
+  }
+}
+
+// Downsweep with node set w from (xf, xl) in thread 0, interior
+// back-substitution, x stored from registers (8 consecutive rows per thread).
+__device__ __forceinline__ void upper_finish(UpperSmem& sm, int w, RegAcc<kUpperM>& regs, real xf, real xl,
+                                             real* x, int64_t n, int64_t t, bool& bad) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  cta_downsweep(xf, xl, sm.tree[w], sm.wnodes[w], lane, warp, kUpperP / 32, kUpperP);
+  block_interior<kUpperM>(regs, kUpperM, xf, xl, bad);
+  const int64_t g0 = t * (kUpperP * kUpperM) + tid * kUpperM;
+#pragma unroll
+  for (int j = 0; j < kUpperM; ++j) {
+    bad |= !isfinite(regs.x(j));
+    if (g0 + j < n) x[g0 + j] = regs.x(j);
+  }
+}
+
+__global__ void __launch_bounds__(kUpperP, 4) upper_fused_kernel(UpperArgs u) {
+  constexpr int T = kUpperP * kUpperM;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  UpperSmem& sm = *reinterpret_cast<UpperSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t t = blockIdx.x;
+  bool bad = false;
+  // Dependents may launch once every CTA of this grid runs (triggered after
+  // the wait: see warp_tile_kernel); the grid is co-resident by construction.
+  pdl_wait();
+  pdl_launch_dependents();
+
+  // ---- level 1, this CTA's tile: reduce, keep rows and tree ----------------
+  const TileCtx ctx = upper_ctx(u.a1, u.b1, u.c1, u.d1, u.n1, t);
+  for (int i = tid; i < T; i += kUpperP) {
+    const bool in = i < ctx.valid;
+    const int64_t g = ctx.row0 + i;
+    sm.rows[0][i] = in ? __ldcg(u.a1 + g) : real(0);
+    sm.rows[1][i] = in ? __ldcg(u.b1 + g) : real(0);
+    sm.rows[2][i] = in ? __ldcg(u.c1 + g) : real(0);
+    sm.rows[3][i] = in ? __ldcg(u.d1 + g) : real(0);
+  }
+  __syncthreads();
+  {
+    RegAcc<kUpperM> regs;
+    regs.load(sm.rows[0], sm.rows[1], sm.rows[2], sm.rows[3], tid * kUpperM, ctx);
+    const Seg seg = block_reduce_fast<kUpperM, false>(regs, bad);
+    const Seg top = cta_upsweep(seg, sm.tree[0], sm.wnodes[0], lane, warp, kUpperP / 32, kUpperP, bad);
+    if (tid == 0) {
+      u.a2[2 * t] = top.F.a; u.b2[2 * t] = top.F.b; u.c2[2 * t] = top.F.c; u.d2[2 * t] = top.F.d;
+      u.a2[2 * t + 1] = top.L.a; u.b2[2 * t + 1] = top.L.b;
+      u.c2[2 * t + 1] = top.L.c; u.d2[2 * t + 1] = top.L.d;
+      __threadfence();
+      const unsigned long long ticket = atomicAdd(u.sync, 1ull);
+      sm.last = (ticket == gridDim.x - 1);
+      if (sm.last) {
+        atomicExch(u.sync, 0ull);
+        __threadfence();
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- level 2 (the last CTA): solve the single tile, release the flag ------
+  if (sm.last) {
+    RegAcc<kUpperM> r2;
+    upper_regs_global(u.a2, u.b2, u.c2, u.d2, u.n2, 0, r2);
+    const Seg s2 = block_reduce_fast<kUpperM, false>(r2, bad);
+    const Seg top2 = cta_upsweep(s2, sm.tree[1], sm.wnodes[1], lane, warp, kUpperP / 32, kUpperP, bad);
+    real xf = 0.0, xl = 0.0;
+    if (tid == 0) {
+      const real det = fma(top2.F.b, top2.L.b, -top2.F.c * top2.L.a);
+      bad |= (det == 0.0);
+      const real inv = drcp(det);
+      xf = fma(top2.F.d, top2.L.b, -top2.F.c * top2.L.d) * inv;
+      xl = fma(top2.F.b, top2.L.d, -top2.L.a * top2.F.d) * inv;
+    }
+    __syncthreads();
+    upper_finish(sm, 1, r2, xf, xl, u.x2, u.n2, 0, bad);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicExch(u.sync + 1, 1ull);  // level 2's x is out
+    }
+  }
+
+  // ---- level 1, this CTA's tile: back-substitute from level 2's x ----------
+  real xf = 0.0, xl = 0.0;
+  if (tid == 0) {
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_gpu_u64(u.sync + 1) == 0) {
+      if (global_ns() - t0 > 1000000000ull) {
+        atomicOr(u.flag, 8);
+        break;
+      }
+      __nanosleep(32);
+    }
+    xf = __ldcg(u.x2 + 2 * t);
+    xl = __ldcg(u.x2 + 2 * t + 1);
+    // the last CTA past the flag re-arms it
+    if (atomicAdd(u.sync + 2, 1ull) == gridDim.x - 1) {
+      atomicExch(u.sync + 1, 0ull);
+      atomicExch(u.sync + 2, 0ull);
+    }
+  }
+  RegAcc<kUpperM> regs;
+  regs.load(sm.rows[0], sm.rows[1], sm.rows[2], sm.rows[3], tid * kUpperM, ctx);
+  __syncthreads();
+  upper_finish(sm, 0, regs, xf, xl, u.x1, u.n1, t, bad);
+  if (bad) atomicOr(u.flag, 1);
+}
+
+int upper_fused_capacity(int sm_count) {
+  const size_t smem = upper_smem_bytes();
+  if (ensure_smem_attr(upper_fused_kernel, smem) != cudaSuccess) return 0;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, upper_fused_kernel, kUpperP, smem) !=
+      cudaSuccess)
+    return 0;
+  return per_sm * sm_count;
+}
+
+cudaError_t launch_upper_fused(const UpperArgs& u, int sm_count, cudaStream_t st, int* grid_out) {
+  constexpr int64_t T = (int64_t)kUpperP * kUpperM;
+  const int64_t tiles = (u.n1 + T - 1) / T;
+  if (u.n2 != 2 * tiles || u.n2 > T) return cudaErrorInvalidValue;
+  if (tiles > upper_fused_capacity(sm_count)) return cudaErrorInvalidConfiguration;
+  // Cooperative launch: the CTAs are scheduled as one gang (the flag wait
+  // needs them co-resident even beside other streams' kernels).
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)tiles);
+  cfg.blockDim = dim3(kUpperP);
+  cfg.dynamicSmemBytes = upper_smem_bytes();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeCooperative;
+  attr[na++].val.cooperative = 1;
+  if (g_use_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (grid_out) *grid_out = (int)tiles;
+  return cudaLaunchKernelEx(&cfg, upper_fused_kernel, u);
 }
 
 // ---------------------------------------------------------------------------

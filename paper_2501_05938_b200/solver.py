@@ -40,6 +40,7 @@ PM_OPT_UPPER_CTA_M = 20
 PM_OPT_UPPER_CTA_P = 21
 PM_OPT_GRAPHS = 22
 PM_OPT_PAIR_STAGES = 23
+PM_OPT_UPPER_FUSED = 24
 PM_MAX_M = 128
 
 

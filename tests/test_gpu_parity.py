@@ -505,9 +505,10 @@ def test_launch_plan_n8e7(solver):
     solver.solve_device(a, b, c, d, m=10)
     solver.check()
     # level 0: warp tiles of 32*10 rows -> 2 rows each; level 1: CTA tiles of
-    # 128*8 rows; level 2 (<= 1024 rows): one ROOT tile
+    # 128*8 rows; level 2 (<= 1024 rows): one ROOT tile.  Launches: Stage 1,
+    # levels 1-2 fused (PM_OPT_UPPER_FUSED), Stage 3
     assert solver.last_plan() == [80_000_000, 500_000, 978]
-    assert solver.last_launch_count == 5
+    assert solver.last_launch_count == 3
 
 
 @pytest.mark.parametrize("warp_tiles", [0, 1])
@@ -522,7 +523,10 @@ def test_level0_kernel_variants(solver, warp_tiles, n, m):
         x = solver.solve_device(a, b, c, d, m=m)
         solver.check()
         plan = solver.last_plan()
-        assert solver.last_launch_count == 2 * len(plan) - 1
+        # REDUCE + SOLVE per level, one ROOT; a three-level plan runs levels
+        # 1-2 in one launch (PM_OPT_UPPER_FUSED)
+        fused = len(plan) == 3 and plan[2] <= 1024
+        assert solver.last_launch_count == 2 * len(plan) - 1 - (2 if fused else 0)
     finally:
         solver.set_option(PM_OPT_WARP_TILES, 1)
     _check(x.cpu().numpy(), *oracle.generate(n, n % 97))
@@ -807,3 +811,98 @@ def test_bench_batch_sharded_path(tmp_path):
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["config"]["systems_per_gpu"] == [5, 4]
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["scaling"] == "strong"
+
+
+# ---- upper levels in one launch (PM_OPT_UPPER_FUSED, default on) -------------
+
+@pytest.mark.parametrize("n,m,fused", [
+    (131_072 * 2, 8, True), (200_003, 10, True), (1_000_037, 10, True), (4_999_999, 16, True),
+    (50_001, 2, True), (3_000_000, 8, True), (150_000, 10, False), (20_000_000, 2, False),
+    (777, 10, False), (83_000_001, 10, True)])
+def test_upper_fused(solver, n, m, fused):
+    """Fused levels 1-2 (one launch instead of three) are bit-identical to the
+    separate REDUCE / ROOT / SOLVE launches and meet the oracle bars."""
+    import torch
+
+    from paper_2501_05938_b200.solver import PM_OPT_UPPER_FUSED
+
+    a, b, c, d = _device_system(solver, n, seed=n % 89)
+    x = solver.solve_device(a, b, c, d, m=m)
+    solver.check()
+    k_fused = solver.last_launch_count
+    solver.set_option(PM_OPT_UPPER_FUSED, 0)
+    try:
+        x2 = solver.solve_device(a, b, c, d, m=m)
+        solver.check()
+        k_sep = solver.last_launch_count
+    finally:
+        solver.set_option(PM_OPT_UPPER_FUSED, 1)
+    assert (k_sep - k_fused == 2) if fused else (k_sep == k_fused)
+    assert torch.equal(x, x2)
+    if n <= 5_000_000:
+        _check(x.cpu().numpy(), *(t.cpu().numpy() for t in (a, b, c, d)))
+    else:  # full-size: residual on the device
+        r = torch.empty_like(x)
+        r[:] = b * x - d
+        r[1:] += a[1:] * x[:-1]
+        r[:-1] += c[:-1] * x[1:]
+        assert (torch.linalg.vector_norm(r) / torch.linalg.vector_norm(d)).item() <= RES_TOL
+
+
+def test_upper_fused_repeated_graphs_and_streams(solver):
+    """The counters re-arm every launch: back-to-back solves, CUDA-graph replays
+    and two handles solving concurrently on two streams (gang-scheduled grids:
+    no flag-wait timeout) all give the same x."""
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.solver import PM_OPT_GRAPHS
+
+    n, m = 2_000_003, 10
+    a, b, c, d = _device_system(solver, n, seed=3)
+    ref = solver.solve_device(a, b, c, d, m=m).clone()
+    solver.check()
+    for _ in range(30):
+        x = solver.solve_device(a, b, c, d, m=m)
+    solver.check()
+    assert torch.equal(x, ref)
+    s = torch.cuda.Stream()
+    solver.set_option(PM_OPT_GRAPHS, 1)
+    try:
+        with torch.cuda.stream(s):
+            for _ in range(30):
+                x = solver.solve_device(a, b, c, d, m=m, stream=s)
+        s.synchronize()
+        solver.check()
+    finally:
+        solver.set_option(PM_OPT_GRAPHS, 0)
+    assert torch.equal(x, ref)
+    other = PartitionSolver(0)
+    try:
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        xs1, xs2 = torch.empty_like(a), torch.empty_like(a)
+        for _ in range(20):
+            solver.solve_device(a, b, c, d, m=m, out=xs1, stream=s1)
+            other.solve_device(a, b, c, d, m=m, out=xs2, stream=s2)
+        torch.cuda.synchronize()
+        solver.check()
+        other.check()
+        assert torch.equal(xs1, ref) and torch.equal(xs2, ref)
+    finally:
+        other.close()
+
+
+def test_upper_fused_row_scaled_retry(solver):
+    """A row-scaled system whose fast path flags a pivot: the robust re-run
+    (classic sweeps, separate upper launches) repairs x."""
+    import torch
+
+    n = 1_000_000
+    a, b, c, d = oracle.generate(n, 11)
+    sc = 10.0 ** np.random.default_rng(5).uniform(-150, 150, n)
+    t = [torch.from_numpy(v * sc).cuda() for v in (a, b, c, d)]
+    xd = solver.solve_device(*t, m=10)
+    solver.check()
+    x = xd.cpu().numpy()
+    assert oracle.rel_err(x, oracle.thomas(a, b, c, d)) <= REL_TOL
+    assert oracle.residual(a, b, c, d, x) <= RES_TOL
