@@ -29,7 +29,7 @@ def main():
 
         s.set_option(PM_OPT_PDL, 0)
     st = torch.cuda.Stream()
-    for n, m in ((70_001, 10), (9_999, 7), (3_000, 16)):
+    for n, m in ((70_001, 10), (200_003, 10), (9_999, 7), (3_000, 16)):  # 200_003: fused upper levels
         a, b, c, d = oracle.generate(n, n)
         t = [torch.from_numpy(v).cuda() for v in (a, b, c, d)]
         with torch.cuda.stream(st):
