@@ -532,28 +532,31 @@ int enq_root(pm_handle_t h, size_t k, cudaStream_t st, int64_t sys_len) {
 }
 
 
-// Levels 1-2 in one launch (pm::launch_upper_fused): a three-level plan with
-// levels 1 and 2 of 128 x 8 CTA tiles, level 2 a single tile, and every
-// level-1 tile's CTA co-resident.  Not in robust mode (classic sweeps).
+// The top two levels in one launch (pm::launch_upper_fused): a plan of three
+// or more levels whose top level is one 128 x 8 CTA tile fed by a level of
+// 128 x 8 CTA tiles with every tile's CTA co-resident (N = 8e7, m = 10:
+// levels 1-2; N = 1e9: levels 2-3).  Not in robust mode (classic sweeps).
 template <class R>
 bool upper_fusable(pm_handle_t h) {
-  if (!h->upper_fused || h->robust_mode || h->chain || h->p2p_top.active || h->levels.size() != 3)
+  if (!h->upper_fused || h->robust_mode || h->chain || h->p2p_top.active || h->levels.size() < 3)
     return false;
   auto cta8 = [](const Level& L) {
     return L.warps_per_cta == 0 && !L.pair && L.P == pm::kUpperP && L.m == pm::kUpperM && L.pad_mode == 1;
   };
-  const Level& L1 = h->levels[1];
-  const Level& L2 = h->levels[2];
-  if (!cta8(L1) || !cta8(L2) || L2.ntiles != 1 || L2.n != 2 * L1.ntiles) return false;
+  const size_t top = h->levels.size() - 1;
+  const Level& Lk = h->levels[top - 1];
+  const Level& Lt = h->levels[top];
+  if (!cta8(Lk) || !cta8(Lt) || Lt.ntiles != 1 || Lt.n != 2 * Lk.ntiles) return false;
   int& cap = h->upper_cap[sizeof(R) == 4];
   if (cap < 0) cap = Prec<R>::upper_capacity(h->sm_count);
-  return L1.ntiles <= cap;
+  return Lk.ntiles <= cap;
 }
 
+// Levels k and k+1 (the top) in one launch.
 template <class R>
-int enq_upper_fused(pm_handle_t h, cudaStream_t st) {
-  const Level& L1 = h->levels[1];
-  const Level& L2 = h->levels[2];
+int enq_upper_fused(pm_handle_t h, size_t k, cudaStream_t st) {
+  const Level& L1 = h->levels[k];
+  const Level& L2 = h->levels[k + 1];
   typename Prec<R>::UpperArgs u;
   u.a1 = static_cast<const R*>(L1.a); u.b1 = static_cast<const R*>(L1.b);
   u.c1 = static_cast<const R*>(L1.c); u.d1 = static_cast<const R*>(L1.d);
@@ -573,20 +576,27 @@ int enq_upper_fused(pm_handle_t h, cudaStream_t st) {
   if (e != cudaSuccess) return cuda_fail(h, e, "fused upper-level kernel launch");
   if (timed) {
     cudaEventRecord(h->kev[ev + 1], st);
-    h->krec.push_back({3, 1, ev});
+    h->krec.push_back({3, (int)k, ev});
   }
   if (grid > 0) ++h->launches;
   return PM_OK;
 }
 
 // Upper levels (1..top) on one stream: REDUCE 1..top-1, ROOT top, SOLVE
-// top-1..1 (chain mode: level 1 is the top, a single ROOT), or the fused
-// single launch when it applies.
+// top-1..1 (chain mode: level 1 is the top, a single ROOT); the top two
+// levels in one launch when that applies.
 template <class R>
 int enq_upper(pm_handle_t h, cudaStream_t st) {
   const size_t top = h->levels.size() - 1;
   int r;
-  if (upper_fusable<R>(h)) return enq_upper_fused<R>(h, st);
+  if (upper_fusable<R>(h)) {
+    for (size_t k = 1; k + 1 < top; ++k)
+      if ((r = enq_reduce<R>(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
+    if ((r = enq_upper_fused<R>(h, top - 1, st))) return r;
+    for (size_t k = top - 1; k-- > 1;)
+      if ((r = enq_solve<R>(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
+    return PM_OK;
+  }
   for (size_t k = 1; k < top; ++k)
     if ((r = enq_reduce<R>(h, k, 0, h->levels[k].ntiles, st, true, true, 0, nullptr))) return r;
   if (top >= 1 && (r = enq_root<R>(h, top, st, 0))) return r;

@@ -6,5 +6,9 @@ except Exception:
     print("ERROR: " + " | ".join(line[-3:]))
     sys.exit(0)
 r = d["roofline"]
-print(f"{d['ms_per_step']:.4f} ms  solve {r['kernel_ms']:.4f} ({r['frac']:.3f})  reduce {r['stage1']['kernel_ms']:.4f} "
-      f"({r['stage1']['frac']:.3f})  whole {r['whole_solve']['frac']:.3f}  kernels {r.get('kernels_ms')}")
+out = f"{d['ms_per_step']:.4f} ms  solve {r.get('kernel_ms', float('nan')):.4f} ({r['frac']:.3f})"
+if "stage1" in r:
+    out += f"  reduce {r['stage1']['kernel_ms']:.4f} ({r['stage1']['frac']:.3f})"
+if "whole_solve" in r:
+    out += f"  whole {r['whole_solve']['frac']:.3f}"
+print(out + f"  kernels {r.get('kernels_ms')}")
