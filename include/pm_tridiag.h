@@ -96,7 +96,7 @@ typedef struct pm_model_bundle {
                                   (default 0 = CTA tiles with m = 8)               */
 #define PM_OPT_ROOT_M 12       /* ROOT tile = 128 * root_m rows (default 8)        */
 #define PM_OPT_PDL 13          /* programmatic dependent launch (process-wide;
-                                  default: on for the FP64 kernels, off for FP32)  */
+                                  default on; 0 disables it for both precisions)   */
 #define PM_OPT_BATCH_CLUSTER 14 /* 1: pm_solve_batch_device_f64 runs one thread-
                                   block cluster per system (all stages while the
                                   system is L2-resident: 40 B/unknown of HBM

@@ -32,15 +32,16 @@
 
 namespace PM_NS {
 
-// Programmatic dependent launch: on for the FP64 kernels, off for FP32, where
-// the early-launched dependents cost 20-35 % of the solve on B200 (round-1
-// sweep: FP32 N = 8e7 0.594 -> 0.573 ms without PDL, pair tiles 0.652 ->
-// 0.481 ms; FP64 within noise either way).
-#ifdef PM_REAL_F32
-bool g_use_pdl = false;
-#else
+// Programmatic dependent launch, on for both precisions.  Every kernel lets
+// its dependents launch only after its own griddepcontrol.wait (so at most the
+// running kernel and its successor are resident, and a Stage-3 launch implies
+// that Stage 1 of its solve passed its wait); Stage 3 and upper-level SOLVEs
+// wait only before reading the level above's x.  Round-1 history: with the
+// dependents triggered before the wait, FP32 lost 20-35 % to PDL (pair tiles
+// 0.652 vs 0.481 ms) and ran without it; with the ordering above FP32 gains
+// 0.5 % (0.4753 -> 0.4730 ms at N = 8e7).  The FP32 non-pair-tile path
+// (PM_OPT_PAIR_TILES=0) is still faster with PDL off (PM_OPT_PDL=0).
 bool g_use_pdl = true;
-#endif
 
 // Launch with the programmatic-stream-serialization attribute (PDL).
 template <class K, class A>
@@ -1071,22 +1072,18 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     fence_mbar_init();
   }
   __syncwarp();
-  pdl_wait();
+  // Stage 3 waits only before reading xb (see warp_tile_kernel)
+  if constexpr (MODE == kModeReduce) pdl_wait();
   pdl_launch_dependents();
   if (lane == 0)
     for (int st = 0; st < S && st < nlocal; ++st) issue(st, tile_of(st));
 
   bool bad = false;
   real xf_next = 0.0, xl_next = 0.0;
-  if (MODE != kModeReduce && nlocal > 0) {
-    const int64_t t0 = tile_of(0);
-    xf_next = __ldg(args.xb + 2 * t0);
-    xl_next = __ldg(args.xb + 2 * t0 + 1);
-  }
   for (int64_t k = 0; k < nlocal; ++k) {
     const int64_t t = tile_of(k);
     const real xf_tile = xf_next, xl_tile = xl_next;
-    if (MODE != kModeReduce && k + 1 < nlocal) {
+    if (MODE != kModeReduce && k > 0 && k + 1 < nlocal) {
       const int64_t tn = tile_of(k + 1);
       xf_next = __ldg(args.xb + 2 * tn);
       xl_next = __ldg(args.xb + 2 * tn + 1);
@@ -1135,6 +1132,16 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     } else {
       warp_upsweep(seg, nodes, lane, nlanes, bad);
       real xf = xf_tile, xl = xl_tile;
+      if (k == 0) {
+        pdl_wait();
+        xf = __ldg(args.xb + 2 * t);
+        xl = __ldg(args.xb + 2 * t + 1);
+        if (nlocal > 1) {
+          const int64_t tn = tile_of(1);
+          xf_next = __ldg(args.xb + 2 * tn);
+          xl_next = __ldg(args.xb + 2 * tn + 1);
+        }
+      }
       __syncwarp();
       warp_downsweep(xf, xl, nodes, lane, nlanes);
       // split the lane's pair: block 0 = [xf, x_last(0)], block 1 = [x_first(1), xl]
