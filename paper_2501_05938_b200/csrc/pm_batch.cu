@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(512, 1) batch_cluster_kernel(BatchArgs args) {
     ctx.zf = true;
     ctx.zl = true;
     ctx.sys_len = 0;
+    ctx.sys_magic = 0;
     return ctx;
   };
 

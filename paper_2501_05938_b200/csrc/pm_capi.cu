@@ -418,6 +418,16 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
   return PM_OK;
 }
 
+// Batch system length of a launch, with the fast-modulo multiplier when the
+// rows and the length fit 32 bits.
+template <class Args>
+void set_sys(Args& A, int64_t sys_len) {
+  A.sys_len = sys_len;
+  A.sys_magic = (sys_len > 0 && A.n < (int64_t(1) << 32) && sys_len < (int64_t(1) << 32))
+                    ? UINT64_MAX / (uint64_t)sys_len + 1
+                    : 0;
+}
+
 template <class R>
 typename Prec<R>::Args args_for(pm_handle_t h, const Level& L, int64_t t0, int64_t t1) {
   typename Prec<R>::Args A;
@@ -501,7 +511,7 @@ int enq_reduce(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st,
   }
   A.zero_first = zf;
   A.zero_last = zl;
-  A.sys_len = (k == 0) ? sys_len : 0;
+  set_sys(A, (k == 0) ? sys_len : 0);
   if (k == 0 && h->chain) set_chain<R>(h, A, part);
   if (h->p2p_top.active && k + 1 == h->levels.size()) set_p2p<R>(h, A);
   return launch<R>(h, pm::kModeReduce, A, L, st);
@@ -516,7 +526,7 @@ int enq_solve(pm_handle_t h, size_t k, int64_t t0, int64_t t1, cudaStream_t st, 
   if (L.warps_per_cta > 0 && h->solve_stages > 0) A.stages = std::min(h->solve_stages, L.stages);
   A.zero_first = zf;
   A.zero_last = zl;
-  A.sys_len = (k == 0) ? sys_len : 0;
+  set_sys(A, (k == 0) ? sys_len : 0);
   A.reverse = h->reverse;
   if (k == 0 && h->chain) set_chain<R>(h, A, part);
   if (h->p2p_top.active && k + 1 == h->levels.size()) set_p2p<R>(h, A);
@@ -527,7 +537,7 @@ template <class R>
 int enq_root(pm_handle_t h, size_t k, cudaStream_t st, int64_t sys_len) {
   const Level& L = h->levels[k];
   typename Prec<R>::Args A = args_for<R>(h, L, 0, 1);
-  A.sys_len = (k == 0) ? sys_len : 0;
+  set_sys(A, (k == 0) ? sys_len : 0);
   return launch<R>(h, pm::kModeRoot, A, L, st);
 }
 
