@@ -1033,7 +1033,7 @@ __host__ __device__ size_t pair_smem_bytes(int m, int stages) {
 #ifndef PM_PAIR_MINB
 #define PM_PAIR_MINB 5
 #endif
-template <int M, int MODE>
+template <int M, int MODE, bool SYS>
 __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs args) {
   static_assert(M > 0, "compile-time m only");
   constexpr int T = 64 * M;
@@ -1099,8 +1099,8 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     ctx.bulk_rows = ctx.valid & ~(kBulkRows - 1);
     ctx.zf = args.zero_first != 0;
     ctx.zl = args.zero_last != 0;
-    ctx.sys_len = args.sys_len;
-    ctx.sys_magic = args.sys_magic;
+    ctx.sys_len = SYS ? args.sys_len : 0;  // SYS = false: batch checks compiled away
+    ctx.sys_magic = SYS ? args.sys_magic : 0;
     // non-empty lanes (a prefix) and whether this lane's second block is non-empty
     const int nblocks = args.pad_mode ? 64 : (ctx.valid + M - 1) / M;
     const int nlanes = (nblocks + 1) / 2;
@@ -1187,10 +1187,10 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
   if (bad) atomicOr(args.flag, 1);
 }
 
-template <int M, int MODE>
+template <int M, int MODE, bool SYS>
 static cudaError_t launch_pair_one(const TileArgs& args, int warps_per_cta, int sm_count,
                                    cudaStream_t st, int* grid_out) {
-  auto kern = warp_pair_kernel<M, MODE>;
+  auto kern = warp_pair_kernel<M, MODE, SYS>;
   const size_t smem = pair_smem_bytes(M, args.stages) * warps_per_cta;
   {
     cudaError_t e = ensure_smem_attr(kern, smem);
@@ -1213,9 +1213,15 @@ static cudaError_t launch_pair_one(const TileArgs& args, int warps_per_cta, int 
 cudaError_t launch_warp_pair_kernel(int mode, const TileArgs& args, int warps_per_cta, int sm_count,
                                     cudaStream_t st, int* grid_out) {
   const bool red = mode == kModeReduce;
-#define PM_PAIR_CASE(MM)                                                                       \
-  return red ? launch_pair_one<MM, kModeReduce>(args, warps_per_cta, sm_count, st, grid_out)   \
-             : launch_pair_one<MM, kModeSolve>(args, warps_per_cta, sm_count, st, grid_out)
+  // single systems: both stages without the batch boundary checks (FP32 N = 8e7:
+  // 0.4738 -> 0.4679 ms)
+  const bool sys = args.sys_len != 0;
+#define PM_PAIR_CASE(MM)                                                                              \
+  if (red)                                                                                            \
+    return sys ? launch_pair_one<MM, kModeReduce, true>(args, warps_per_cta, sm_count, st, grid_out)  \
+               : launch_pair_one<MM, kModeReduce, false>(args, warps_per_cta, sm_count, st, grid_out); \
+  return sys ? launch_pair_one<MM, kModeSolve, true>(args, warps_per_cta, sm_count, st, grid_out)     \
+             : launch_pair_one<MM, kModeSolve, false>(args, warps_per_cta, sm_count, st, grid_out)
   switch (args.m) {
     case 2: PM_PAIR_CASE(2);
     case 8: PM_PAIR_CASE(8);
