@@ -230,7 +230,7 @@ __device__ bool p2p_chain(const TileArgs& A, real& xf, real& xl, bool& bad) {
 // ---------------------------------------------------------------------------
 // The tile kernel
 // ---------------------------------------------------------------------------
-template <int M, int MODE, bool BULK>
+template <int M, int MODE, bool BULK, bool SYS>
 __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t bars[kMaxStages];
@@ -298,8 +298,8 @@ __global__ void __launch_bounds__(256) tile_kernel(TileArgs args) {
     ctx.bulk_rows = BULK ? (ctx.valid & ~(kBulkRows - 1)) : ctx.valid;
     ctx.zf = args.zero_first != 0;
     ctx.zl = args.zero_last != 0;
-    ctx.sys_len = args.sys_len;
-    ctx.sys_magic = args.sys_magic;
+    ctx.sys_len = SYS ? args.sys_len : 0;  // SYS = false: the upper levels' build
+    ctx.sys_magic = SYS ? args.sys_magic : 0;
     // non-empty leaf blocks of this tile (pad mode: all P)
     const int nblk = args.pad_mode ? P : (ctx.valid + m - 1) / m;
     real* sa = stage_ptr(s, 0);
@@ -1441,10 +1441,10 @@ size_t tile_smem_bytes(int mode, int P, int m, int stages) {
   return bytes;
 }
 
-template <int M, int MODE, bool BULK>
+template <int M, int MODE, bool BULK, bool SYS = true>
 static cudaError_t launch_one(const TileArgs& args, int P, int sm_count, cudaStream_t st,
                               int* grid_out) {
-  auto kern = tile_kernel<M, MODE, BULK>;
+  auto kern = tile_kernel<M, MODE, BULK, SYS>;
   const int S = BULK ? args.stages : 1;
   const size_t smem = tile_smem_bytes(MODE, P, (M > 0 ? M : args.m), S);
   {
@@ -1467,9 +1467,16 @@ static cudaError_t launch_one(const TileArgs& args, int P, int sm_count, cudaStr
 template <int MODE, bool BULK>
 static cudaError_t dispatch_m(int Mspec, const TileArgs& args, int P, int sm_count,
                               cudaStream_t st, int* grid_out) {
+  // upper levels (m = 8, ragged m = 2; no system boundaries): the build
+  // without the batch boundary checks
+  const bool nosys = BULK && args.sys_len == 0;
   switch (Mspec) {
-    case 2: return launch_one<2, MODE, BULK>(args, P, sm_count, st, grid_out);
-    case 8: return launch_one<8, MODE, BULK>(args, P, sm_count, st, grid_out);
+    case 2:
+      return nosys ? launch_one<2, MODE, BULK, false>(args, P, sm_count, st, grid_out)
+                   : launch_one<2, MODE, BULK>(args, P, sm_count, st, grid_out);
+    case 8:
+      return nosys ? launch_one<8, MODE, BULK, false>(args, P, sm_count, st, grid_out)
+                   : launch_one<8, MODE, BULK>(args, P, sm_count, st, grid_out);
     case 10: return launch_one<10, MODE, BULK>(args, P, sm_count, st, grid_out);
     case 16: return launch_one<16, MODE, BULK>(args, P, sm_count, st, grid_out);
     default: return launch_one<0, MODE, BULK>(args, P, sm_count, st, grid_out);
