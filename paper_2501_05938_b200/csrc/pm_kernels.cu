@@ -846,7 +846,9 @@ __global__ void __launch_bounds__(128, (MODE == kModeReduce ? PM_REDUCE_MINB : P
     ctx.zl = args.zero_last != 0;
     ctx.sys_len = SYS ? args.sys_len : 0;  // SYS = false: the batch checks compile away
     ctx.sys_magic = SYS ? args.sys_magic : 0;
-    const int nblk = args.pad_mode ? 32 : (ctx.valid + m - 1) / m;
+    // SYS = false is only launched for padded tiles: a constant 32 folds the
+    // trees' bounds checks away
+    const int nblk = (!SYS || args.pad_mode) ? 32 : (ctx.valid + m - 1) / m;
     real* sa = stage_ptr(s, 0);
     real* sb = stage_ptr(s, 1);
     real* sc = stage_ptr(s, 2);
@@ -1280,12 +1282,13 @@ static cudaError_t launch_warp_m(int mode, const TileArgs& args, int warps_per_c
 
 cudaError_t launch_warp_tile_kernel(int mode, const TileArgs& args, int warps_per_cta,
                                     int sm_count, cudaStream_t st, int* grid_out) {
-  // SYS = false compiles the batch boundary checks away: Stage 3 of a single
-  // system then runs with 110 instead of 128 registers (0.508 -> 0.492 ms at
-  // N = 8e7); Stage 1 keeps the general variant (its SYS = false build is
-  // slower: 0.378 -> 0.421 ms, a worse schedule at 203 registers).
+  // SYS = false (single padded system) compiles the batch boundary checks and
+  // the ragged-tile bounds away: Stage 3 of a single system then runs with 106
+  // instead of 128 registers (0.508 -> 0.4895 ms at N = 8e7); Stage 1 keeps
+  // the general variant (its SYS = false build is slower: 0.378 -> 0.421 ms,
+  // a worse schedule at 203 registers).
   if (args.nchunks > 0) return launch_warp_m<true, true>(mode, args, warps_per_cta, sm_count, st, grid_out);
-  return (args.sys_len || mode == kModeReduce)
+  return (args.sys_len || !args.pad_mode || mode == kModeReduce)
              ? launch_warp_m<false, true>(mode, args, warps_per_cta, sm_count, st, grid_out)
              : launch_warp_m<false, false>(mode, args, warps_per_cta, sm_count, st, grid_out);
 }
