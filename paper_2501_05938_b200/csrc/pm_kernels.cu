@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(64, PM_PAIR_MINB) warp_pair_kernel(TileArgs ar
     ctx.sys_len = SYS ? args.sys_len : 0;  // SYS = false: batch checks compiled away
     ctx.sys_magic = SYS ? args.sys_magic : 0;
     // non-empty lanes (a prefix) and whether this lane's second block is non-empty
-    const int nblocks = args.pad_mode ? 64 : (ctx.valid + M - 1) / M;
+    const int nblocks = (!SYS || args.pad_mode) ? 64 : (ctx.valid + M - 1) / M;  // SYS = false: padded
     const int nlanes = (nblocks + 1) / 2;
     const bool has2 = 2 * lane + 1 < nblocks;
     const int sidx = static_cast<int>(k % S);
@@ -1215,9 +1215,9 @@ static cudaError_t launch_pair_one(const TileArgs& args, int warps_per_cta, int 
 cudaError_t launch_warp_pair_kernel(int mode, const TileArgs& args, int warps_per_cta, int sm_count,
                                     cudaStream_t st, int* grid_out) {
   const bool red = mode == kModeReduce;
-  // single systems: both stages without the batch boundary checks (FP32 N = 8e7:
-  // 0.4738 -> 0.4679 ms)
-  const bool sys = args.sys_len != 0;
+  // single padded systems: both stages without the batch boundary checks and
+  // the ragged-tile bounds (FP32 N = 8e7: 0.4738 -> 0.4679 ms)
+  const bool sys = args.sys_len != 0 || !args.pad_mode;
 #define PM_PAIR_CASE(MM)                                                                              \
   if (red)                                                                                            \
     return sys ? launch_pair_one<MM, kModeReduce, true>(args, warps_per_cta, sm_count, st, grid_out)  \
