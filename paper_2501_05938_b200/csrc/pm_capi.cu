@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <functional>
 #include <type_traits>
 #include <cmath>
@@ -32,6 +33,9 @@
 #include "streamtune/predictor.hpp"
 
 namespace {
+
+// bumped whenever PM_OPT_PDL changes the process-wide launch attribute
+std::atomic<uint64_t> g_pdl_gen{0};
 
 
 struct Level {
@@ -207,7 +211,7 @@ struct pm_handle_s {
     const void* p[5];
     int64_t n, nps;
     int m;
-    uint64_t gen;
+    uint64_t gen, pdl_gen;
     const void* scratch;
     cudaGraphExec_t exec;
     int launches;
@@ -706,6 +710,7 @@ int run_maybe_graph(pm_handle_t h, cudaStream_t st, size_t esz, const void* cons
   if (!h->use_graphs || h->ktimes || h->robust_mode || st == nullptr) return enqueue();
   for (auto& g : h->graphs) {
     if (g.esz == esz && g.n == n && g.nps == nps && g.m == m && g.gen == h->plan_gen &&
+        g.pdl_gen == g_pdl_gen.load(std::memory_order_relaxed) &&
         g.scratch == h->scratch && std::equal(ptrs, ptrs + 5, g.p)) {
       g.last_use = ++h->graph_clock;
       h->launches = g.launches;
@@ -743,6 +748,7 @@ int run_maybe_graph(pm_handle_t h, cudaStream_t st, size_t esz, const void* cons
   g.nps = nps;
   g.m = m;
   g.gen = h->plan_gen;
+  g.pdl_gen = g_pdl_gen.load(std::memory_order_relaxed);
   g.scratch = h->scratch;
   g.exec = exec;
   g.launches = h->launches;
@@ -1235,7 +1241,9 @@ int dist_solve_p2p_impl(pm_handle_t h, const R* a, const R* b, const R* c, const
     return fail(h, PM_ERR_VALIDATION, "pm_dist_exchange_alloc / pm_dist_set_peers not called");
   if (h->epoch == 0) return fail(h, PM_ERR_VALIDATION, "pm_dist_reduce_p2p must precede the solve");
   const R* slots = reinterpret_cast<const R*>(h->xbuf);
-  const uint64_t* flags = reinterpret_cast<const uint64_t*>(slots + (size_t)2 * h->xworld * 8);
+  // flags at a fixed byte offset for both precisions (exchange_bytes)
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(static_cast<const char*>(h->xbuf) +
+                                                            (size_t)2 * h->xworld * 8 * sizeof(double));
   return dist_solve_impl<R>(h, a, b, c, d, x, n_local, m, h->xrank, h->xworld, slots, stream, flags,
                             h->epoch);
 }
@@ -1318,8 +1326,11 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       h->solve_stages = (int)value;
       return PM_OK;
     case PM_OPT_PDL:
+      // process-wide launch attribute: every handle's recorded graphs carry
+      // the old attribute, so the global generation invalidates them all
       pm::set_pdl(value != 0);
       pm32::set_pdl(value != 0);
+      g_pdl_gen.fetch_add(1, std::memory_order_relaxed);
       return PM_OK;
     case PM_OPT_CHAIN:
       h->opt_chain = value ? 1 : 0;

@@ -163,6 +163,21 @@ __device__ __forceinline__ uint64_t global_ns() {
 }
 
 constexpr int kMaxP2PWorld = 64;
+// Level-2 flag wait of the fused upper levels: generous (the same 20 s as the
+// P2P wait) so a preempted / time-sliced context is not reported as a failure.
+constexpr uint64_t kFusedWaitTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+// Exchange buffer: [2][world][8] reals (slots sized for FP64; FP32 uses the
+// first half) | [2][world] uint64 epoch flags.  The flags sit at the same BYTE
+// offset for both precisions, so a session mixing FP64 and FP32 solves (e.g.
+// the FP64 self-test, then FP32 solves) never reads slot data as a flag.
+__device__ __forceinline__ uint64_t* p2p_flags(void* buf, int world) {
+  return reinterpret_cast<uint64_t*>(static_cast<char*>(buf) + (size_t)2 * world * 8 * sizeof(double));
+}
+__device__ __forceinline__ const uint64_t* p2p_flags(const void* buf, int world) {
+  return reinterpret_cast<const uint64_t*>(static_cast<const char*>(buf) +
+                                           (size_t)2 * world * 8 * sizeof(double));
+}
 
 // Thread 0 of a rank's top-level REDUCE: publish the rank's two interface rows
 // (layout per rank [Fa, La, Fb, Lb, Fc, Lc, Fd, Ld]) into every peer.
@@ -176,8 +191,7 @@ __device__ void p2p_publish(const Seg& top, const TileArgs& A) {
   }
   __threadfence_system();
   for (int k = 0; k < A.xworld; ++k) {
-    uint64_t* flags =
-        reinterpret_cast<uint64_t*>(static_cast<real*>(A.xpeers[k]) + (size_t)2 * A.xworld * 8);
+    uint64_t* flags = p2p_flags(A.xpeers[k], A.xworld);
     st_release_sys(flags + par * A.xworld + A.xrank, A.xepoch);
   }
 }
@@ -188,8 +202,7 @@ __device__ void p2p_publish(const Seg& top, const TileArgs& A) {
 __device__ bool p2p_chain(const TileArgs& A, real& xf, real& xl, bool& bad) {
   const int W = A.xworld, par = static_cast<int>(A.xepoch & 1);
   const real* iface = static_cast<const real*>(A.xlocal) + (size_t)par * W * 8;
-  const uint64_t* flags = reinterpret_cast<const uint64_t*>(static_cast<const real*>(A.xlocal) +
-                                                            (size_t)2 * W * 8);
+  const uint64_t* flags = p2p_flags(A.xlocal, W);
   const uint64_t t0 = global_ns();
   for (int k = 0; k < W; ++k) {
     while (ld_acquire_sys(flags + par * W + k) < A.xepoch) {
@@ -566,7 +579,7 @@ __global__ void __launch_bounds__(kUpperP, 4) upper_fused_kernel(UpperArgs u) {
   if (tid == 0) {
     const uint64_t t0 = global_ns();
     while (ld_acquire_gpu_u64(u.sync + 1) == 0) {
-      if (global_ns() - t0 > 1000000000ull) {
+      if (global_ns() - t0 > kFusedWaitTimeoutNs) {
         atomicOr(u.flag, 8);
         break;
       }

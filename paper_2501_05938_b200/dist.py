@@ -188,7 +188,19 @@ class DistributedSolver:
         if self.iface.dtype != b.dtype:  # FP32 solve: interface equations in FP32
             self.iface = self.iface.to(b.dtype)
             self.iface_all = self.iface_all.to(b.dtype)
-        self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
-        self._all_gather()
-        self.solver.dist_solve(a, b, c, d, x, m, self.rank, self.world, self.iface_all, stream=stream)
+        import contextlib
+
+        import torch
+
+        # the exchange runs on the solve's stream: NCCL (and gloo's .cpu()) order
+        # against the current stream, which must be the one dist_reduce wrote
+        # iface on and dist_solve reads iface_all on
+        if isinstance(stream, int):  # raw cudaStream_t
+            stream = torch.cuda.ExternalStream(stream, device=self.iface.device)
+        ctx = (torch.cuda.stream(stream) if stream is not None and self.iface.is_cuda
+               else contextlib.nullcontext())
+        with ctx:
+            self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
+            self._all_gather()
+            self.solver.dist_solve(a, b, c, d, x, m, self.rank, self.world, self.iface_all, stream=stream)
         return x

@@ -74,7 +74,7 @@ def _suffix(dtype) -> str:
     raise ValidationError("arrays must be float64 or float32")
 
 
-def _dev_ptr(t, n: Optional[int] = None, dtype=None) -> int:
+def _dev_ptr(t, n: Optional[int] = None, dtype=None, device: Optional[int] = None) -> int:
     import torch
 
     dtype = dtype if dtype is not None else torch.float64
@@ -84,6 +84,8 @@ def _dev_ptr(t, n: Optional[int] = None, dtype=None) -> int:
         raise ValidationError("device arrays must be contiguous")
     if n is not None and t.numel() < n:
         raise ValidationError("device array shorter than n")
+    if device is not None and t.device.index != device:
+        raise ValidationError(f"device array on cuda:{t.device.index}, the solver's handle is on cuda:{device}")
     return t.data_ptr()
 
 
@@ -118,6 +120,10 @@ class PartitionSolver:
         self.set_option(PM_OPT_TIMINGS, int(timings))
 
     # -- plumbing -------------------------------------------------------------
+    def _ptr(self, t, n: Optional[int] = None, dtype=None) -> int:
+        """Device pointer of `t`, validated to live on this handle's device."""
+        return _dev_ptr(t, n, dtype, int(self.device))
+
     def _ok(self, st: int):
         if st != 0:
             raise_for(st, self._L.pm_last_error(self._h).decode(errors="replace"))
@@ -184,8 +190,8 @@ class PartitionSolver:
         fn = getattr(self._L, "pm_solve_device_" + _suffix(dt))
         n = int(b.numel()) if n is None else n
         x = out if out is not None else torch.empty(n, dtype=dt, device=b.device)
-        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
-                    _dev_ptr(x, n, dt), n, m, _stream_handle(stream)))
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt),
+                    self._ptr(x, n, dt), n, m, _stream_handle(stream)))
         return x
 
     def solve_batch_device(self, a, b, c, d, n_per_system: int, m: int = 10, out=None, stream=None):
@@ -197,8 +203,8 @@ class PartitionSolver:
         if n_per_system < 1 or n % n_per_system:
             raise ValidationError("array length must be a multiple of n_per_system")
         x = out if out is not None else torch.empty(n, dtype=dt, device=b.device)
-        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
-                    _dev_ptr(x, n, dt), n_per_system, n // n_per_system, m, _stream_handle(stream)))
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt),
+                    self._ptr(x, n, dt), n_per_system, n // n_per_system, m, _stream_handle(stream)))
         return x
 
     def solve_batch_host(self, a, b, c, d, n_per_system: int, m: int = 10, depth: int = 0,
@@ -241,7 +247,7 @@ class PartitionSolver:
         if arrays is None:
             arrays = [torch.empty(count, dtype=dtype, device=dev) for _ in range(4)]
         fn = getattr(self._L, "pm_generate_range_" + _suffix(dtype))
-        self._ok(fn(self._h, *[_dev_ptr(t, count, dtype) for t in arrays], n_total, row0, count, seed,
+        self._ok(fn(self._h, *[self._ptr(t, count, dtype) for t in arrays], n_total, row0, count, seed,
                     _stream_handle(stream)))
         return arrays
 
@@ -267,14 +273,14 @@ class PartitionSolver:
     def dist_reduce(self, a, b, c, d, m: int, rank: int, world: int, iface, stream=None):
         n, dt = int(b.numel()), b.dtype
         fn = getattr(self._L, "pm_dist_reduce_" + _suffix(dt))
-        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt), n,
-                    m, rank, world, _dev_ptr(iface, 8, dt), _stream_handle(stream)))
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt), n,
+                    m, rank, world, self._ptr(iface, 8, dt), _stream_handle(stream)))
 
     def dist_solve(self, a, b, c, d, x, m: int, rank: int, world: int, iface_all, stream=None):
         n, dt = int(b.numel()), b.dtype
         fn = getattr(self._L, "pm_dist_solve_" + _suffix(dt))
-        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
-                    _dev_ptr(x, n, dt), n, m, rank, world, _dev_ptr(iface_all, 8 * world, dt),
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt),
+                    self._ptr(x, n, dt), n, m, rank, world, self._ptr(iface_all, 8 * world, dt),
                     _stream_handle(stream)))
 
     # -- P2P interface exchange (NVLink peer memory; include/pm_tridiag.h) -------
@@ -291,14 +297,14 @@ class PartitionSolver:
     def dist_reduce_p2p(self, a, b, c, d, m: int, stream=None):
         n, dt = int(b.numel()), b.dtype
         fn = getattr(self._L, "pm_dist_reduce_p2p_" + _suffix(dt))
-        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt), n,
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt), n,
                     m, _stream_handle(stream)))
 
     def dist_solve_p2p(self, a, b, c, d, x, m: int, stream=None):
         n, dt = int(b.numel()), b.dtype
         fn = getattr(self._L, "pm_dist_solve_p2p_" + _suffix(dt))
-        self._ok(fn(self._h, _dev_ptr(a, n, dt), _dev_ptr(b, n, dt), _dev_ptr(c, n, dt), _dev_ptr(d, n, dt),
-                    _dev_ptr(x, n, dt), n, m, _stream_handle(stream)))
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt),
+                    self._ptr(x, n, dt), n, m, _stream_handle(stream)))
 
     # -- stream-count model -------------------------------------------------------
     def set_model_bundle(self, bundle: "ModelBundleC"):
