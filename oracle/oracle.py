@@ -24,7 +24,8 @@ REF_PATH = HERE / "_ref" / "libstreamtune_ref.so"
 
 __all__ = [
     "build_oracle", "lib", "ref_lib", "generate", "generate_np", "thomas", "partition_solve",
-    "residual", "rel_err", "dgtsv", "thomas_np", "max_threads",
+    "residual", "rel_err", "dgtsv", "thomas_np", "max_threads", "generate_range", "check_generated",
+    "finish_check",
 ]
 
 _lib = None
@@ -45,6 +46,11 @@ def lib():
         L = C.CDLL(str(LIB_PATH))
         L.orc_generate.argtypes = [_D, _D, _D, _D, C.c_int64, C.c_uint64]
         L.orc_generate.restype = None
+        L.orc_generate_range.argtypes = [_D, _D, _D, _D, C.c_int64, C.c_int64, C.c_int64, C.c_uint64]
+        L.orc_generate_range.restype = None
+        L.orc_check_generated.argtypes = [_D, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_double,
+                                          C.c_double, C.c_int64, C.c_int64, _D]
+        L.orc_check_generated.restype = C.c_int
         L.orc_thomas.argtypes = [_D, _D, _D, _D, _D, _D, C.c_int64]
         L.orc_thomas.restype = C.c_int
         L.orc_partition_workspace.argtypes = [C.c_int64, C.c_int32]
@@ -104,6 +110,40 @@ def generate(n: int, seed: int = 42):
     a, b, c, d = (np.empty(n, np.float64) for _ in range(4))
     lib().orc_generate(_p(a), _p(b), _p(c), _p(d), n, seed)
     return a, b, c, d
+
+
+def generate_range(n_total: int, row0: int, count: int, seed: int = 42):
+    """Rows [row0, row0 + count) of the n_total-row generated system."""
+    a, b, c, d = (np.empty(count, np.float64) for _ in range(4))
+    lib().orc_generate_range(_p(a), _p(b), _p(c), _p(d), n_total, row0, count, seed)
+    return a, b, c, d
+
+
+def check_generated(x, n_total: int, row0: int = 0, seed: int = 42, xl: float = 0.0, xr: float = 0.0,
+                    chunk: int = 1 << 18, pad: int = 1024) -> dict:
+    """Windowed Thomas check of x = rows [row0, row0+len(x)) of the generated
+    system (orc_check_generated): no copy of the system is held.  Returns the
+    parts of the two bars so ranks can combine them:
+    rel_err = max_err / max_ref (max over ranks), residual =
+    sqrt(sum rsq / sum dsq) (sums over ranks)."""
+    x = np.ascontiguousarray(x, np.float64)
+    out = np.zeros(4, np.float64)
+    st = lib().orc_check_generated(_p(x), n_total, row0, len(x), seed, float(xl), float(xr), chunk, pad,
+                                   _p(out))
+    if st != 0:
+        raise ArithmeticError(f"oracle windowed check failed with status {st}")
+    r = {"max_err": float(out[0]), "max_ref": float(out[1]), "rsq": float(out[2]), "dsq": float(out[3])}
+    return finish_check([r])
+
+
+def finish_check(parts) -> dict:
+    """Combine per-rank check_generated parts into the two bars."""
+    me = max(p["max_err"] for p in parts)
+    mr = max(p["max_ref"] for p in parts)
+    rs = sum(p["rsq"] for p in parts)
+    ds = sum(p["dsq"] for p in parts)
+    return {"max_err": me, "max_ref": mr, "rsq": rs, "dsq": ds,
+            "rel_err": me / mr if mr > 0 else me, "residual": float(np.sqrt(rs / ds)) if ds > 0 else float(np.sqrt(rs))}
 
 
 # ---- numpy restatement of the generator (cross-checks the C one) -------------

@@ -58,23 +58,31 @@ static inline double orc_unit(uint64_t key, uint64_t i) {
   return (double)(orc_splitmix64(key + i) >> 11) * 0x1.0p-53;
 }
 
-/* a,c ~ U(-1,1) with a[0] = c[n-1] = 0; b = +-(|a|+|c|+1+U(0,1)); d ~ U(-1,1).
- * Any of the output pointers may be NULL. */
-ORC_API void orc_generate(double* a, double* b, double* c, double* d, int64_t n, uint64_t seed) {
+/* Row i of the n_total-row system: a,c ~ U(-1,1) with a[0] = c[n_total-1] = 0;
+ * b = +-(|a|+|c|+1+U(0,1)); d ~ U(-1,1).  Rows [row0, row0+count) are written
+ * to a[0..count) etc. (a rank's slice of a row-sharded system; identical to
+ * pm_generate_range_f64).  Any of the output pointers may be NULL. */
+ORC_API void orc_generate_range(double* a, double* b, double* c, double* d, int64_t n_total,
+                                int64_t row0, int64_t count, uint64_t seed) {
   const uint64_t ka = orc_stream_key(seed, 0), kc = orc_stream_key(seed, 1);
   const uint64_t kb = orc_stream_key(seed, 2), kd = orc_stream_key(seed, 3);
   const uint64_t ks = orc_stream_key(seed, 4);
 #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < n; ++i) {
+  for (int64_t k = 0; k < count; ++k) {
+    const int64_t i = row0 + k;
     double ai = (i == 0) ? 0.0 : 2.0 * orc_unit(ka, (uint64_t)i) - 1.0;
-    double ci = (i == n - 1) ? 0.0 : 2.0 * orc_unit(kc, (uint64_t)i) - 1.0;
+    double ci = (i == n_total - 1) ? 0.0 : 2.0 * orc_unit(kc, (uint64_t)i) - 1.0;
     double mag = ((fabs(ai) + fabs(ci)) + 1.0) + orc_unit(kb, (uint64_t)i);
     double bi = (orc_splitmix64(ks + (uint64_t)i) >> 63) ? -mag : mag;
-    if (a) a[i] = ai;
-    if (b) b[i] = bi;
-    if (c) c[i] = ci;
-    if (d) d[i] = 2.0 * orc_unit(kd, (uint64_t)i) - 1.0;
+    if (a) a[k] = ai;
+    if (b) b[k] = bi;
+    if (c) c[k] = ci;
+    if (d) d[k] = 2.0 * orc_unit(kd, (uint64_t)i) - 1.0;
   }
+}
+
+ORC_API void orc_generate(double* a, double* b, double* c, double* d, int64_t n, uint64_t seed) {
+  orc_generate_range(a, b, c, d, n, 0, n, seed);
 }
 
 /* ------------------------------------------------------------------ */
@@ -260,6 +268,82 @@ ORC_API double orc_rel_err(const double* x, const double* xr, int64_t n) {
   }
   if (den == 0.0) return num;
   return num / den;
+}
+
+/* ------------------------------------------------------------------ */
+/* Windowed check of a solution of the generated system               */
+/* ------------------------------------------------------------------ */
+/* x[0..count) claims to solve rows [row0, row0+count) of the n_total-row
+ * generated system (seed); xl = x[row0-1] and xr = x[row0+count] (ignored at
+ * the system's ends).  Without holding the system in memory, every window of
+ * `chunk` rows is checked against sequential Thomas on the window widened by
+ * `pad` rows each side (truncated at the system's ends): the synthetic
+ * systems are strictly diagonally dominant with margin >= 1 and |a|+|c| < 2,
+ * so the truncation perturbs the window's centre by < (2/3)^pad relative
+ * (pad = 1024: < 1e-180), far below FP64 rounding -- the centre IS the
+ * Thomas solution of the whole system to the last bit in practice
+ * (tests/test_oracle.py compares it with a whole-system Thomas).
+ * out[0] = max|x - x_thomas|, out[1] = max|x_thomas|,
+ * out[2] = sum (Ax - d)^2, out[3] = sum d^2 over the rows.  Returns 0, 1 on
+ * bad arguments / allocation failure, 2 on a pivot failure. */
+ORC_API int orc_check_generated(const double* x, int64_t n_total, int64_t row0, int64_t count,
+                                uint64_t seed, double xl, double xr, int64_t chunk, int64_t pad,
+                                double* out) {
+  if (count < 1 || row0 < 0 || row0 + count > n_total || chunk < 1 || pad < 0) return 1;
+  const int64_t nch = (count + chunk - 1) / chunk;
+  double emax = 0.0, rmax = 0.0;
+  long double rsq = 0.0L, dsq = 0.0L;
+  int status = 0;
+#pragma omp parallel reduction(max : emax, rmax) reduction(+ : rsq, dsq) reduction(max : status)
+  {
+    const int64_t wmax = chunk + 2 * pad;
+    double* buf = (double*)malloc(sizeof(double) * 6 * (size_t)wmax);
+    if (!buf) status = 1;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t k = 0; k < nch; ++k) {
+      if (!buf) continue;
+      const int64_t lo = row0 + k * chunk;                           /* window, global rows */
+      const int64_t hi = (lo + chunk < row0 + count) ? lo + chunk : row0 + count;
+      const int64_t wlo = (lo - pad > 0) ? lo - pad : 0;               /* widened window */
+      const int64_t whi = (hi + pad < n_total) ? hi + pad : n_total;
+      const int64_t w = whi - wlo;
+      double *a = buf, *b = buf + wmax, *c = buf + 2 * wmax, *d = buf + 3 * wmax;
+      double *xt = buf + 4 * wmax, *work = buf + 5 * wmax;
+      orc_generate_range(a, b, c, d, n_total, wlo, w, seed);
+      a[0] = 0.0;       /* truncation: the window is a system of its own */
+      c[w - 1] = 0.0;
+      /* restore the true couplings for the residual below */
+      double a_lo = 0.0, c_hi = 0.0;
+      if (wlo > 0) orc_generate_range(&a_lo, NULL, NULL, NULL, n_total, wlo, 1, seed);
+      if (whi < n_total) orc_generate_range(NULL, NULL, &c_hi, NULL, n_total, whi - 1, 1, seed);
+      if (orc_thomas(a, b, c, d, xt, work, w) != 0) {
+        status = 2;
+        continue;
+      }
+      a[0] = a_lo;
+      c[w - 1] = c_hi;
+      for (int64_t i = lo; i < hi; ++i) {
+        const int64_t j = i - wlo, q = i - row0;
+        double e = fabs(x[q] - xt[j]);
+        if (isnan(e)) e = INFINITY;
+        if (e > emax) emax = e;
+        if (fabs(xt[j]) > rmax) rmax = fabs(xt[j]);
+        const double xm = (i == 0) ? 0.0 : (q > 0 ? x[q - 1] : xl);
+        const double xp = (i == n_total - 1) ? 0.0 : (q + 1 < count ? x[q + 1] : xr);
+        long double r = (long double)b[j] * x[q] - (long double)d[j];
+        if (i > 0) r += (long double)a[j] * xm;
+        if (i < n_total - 1) r += (long double)c[j] * xp;
+        rsq += r * r;
+        dsq += (long double)d[j] * d[j];
+      }
+    }
+    free(buf);
+  }
+  out[0] = emax;
+  out[1] = rmax;
+  out[2] = (double)rsq;
+  out[3] = (double)dsq;
+  return status;
 }
 
 ORC_API int orc_max_threads(void) {

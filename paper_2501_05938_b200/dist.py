@@ -62,6 +62,7 @@ class DistributedSolver:
         self.iface = torch.zeros(8, dtype=torch.float64, device=dev)
         self.iface_all = torch.zeros(8 * self.world, dtype=torch.float64, device=dev)
         self._opened = []
+        self.last_launches = 0
         self.exchange = "collective"
         if exchange in ("auto", "p2p"):
             if self._setup_p2p():
@@ -183,7 +184,9 @@ class DistributedSolver:
     def solve(self, a, b, c, d, x, m: int = 10, stream=None):
         if self.exchange == "p2p":
             self.solver.dist_reduce_p2p(a, b, c, d, m, stream=stream)
+            k = self.solver.last_launch_count
             self.solver.dist_solve_p2p(a, b, c, d, x, m, stream=stream)
+            self.last_launches = k + self.solver.last_launch_count
             return x
         if self.iface.dtype != b.dtype:  # FP32 solve: interface equations in FP32
             self.iface = self.iface.to(b.dtype)
@@ -201,6 +204,9 @@ class DistributedSolver:
                else contextlib.nullcontext())
         with ctx:
             self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
+            k = self.solver.last_launch_count
             self._all_gather()
             self.solver.dist_solve(a, b, c, d, x, m, self.rank, self.world, self.iface_all, stream=stream)
+        # the solver's own kernels (the all-gather's NCCL kernel is not counted)
+        self.last_launches = k + self.solver.last_launch_count
         return x

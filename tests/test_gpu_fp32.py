@@ -172,3 +172,50 @@ def test_f32_dtype_mismatch_rejected(solver):
     t[0] = t[0].double()
     with pytest.raises(errors.ValidationError):
         solver.solve_device(*t, m=10)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_f32_p2p_mixed_precision_session(solver, world):
+    """P2P exchange in a session that mixes precisions: an FP64
+    solve (the DistributedSolver self-test runs one), then FP32 solves on both
+    buffer parities, then FP64 again.  The epoch flags live at a fixed byte
+    offset, so FP64 slot data is never read as an FP32 session's flags."""
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.dist import split_rows
+
+    handles = [solver] + [PartitionSolver(0) for _ in range(world - 1)]
+    bufs = [h.dist_exchange_alloc(world) for h in handles]
+    for r, h in enumerate(handles):
+        h.dist_set_peers(bufs, r)
+    n, m = 200_003, 10
+    rows = split_rows(n, world, m)
+    offs = np.concatenate([[0], np.cumsum(rows)])
+    sys64 = oracle.generate(n, 31)
+    sys32 = _f32_system(n, 31)
+
+    def run(system, dt):
+        loc = [[torch.from_numpy(np.ascontiguousarray(v[offs[r]:offs[r + 1]])).cuda() for v in system]
+               for r in range(world)]
+        for r in range(world):
+            handles[r].dist_reduce_p2p(*loc[r], m=m)
+        xs = []
+        for r in range(world):
+            x = torch.empty(rows[r], dtype=dt, device="cuda")
+            handles[r].dist_solve_p2p(*loc[r], x, m=m)
+            xs.append(x)
+        for h in handles:
+            h.check()
+        return torch.cat(xs).cpu().numpy()
+
+    for dt in (torch.float64, torch.float32, torch.float32, torch.float32, torch.float64):
+        if dt == torch.float64:
+            a, b, c, d = sys64
+            x = run(sys64, dt)
+            xref = oracle.thomas(a, b, c, d)
+            assert oracle.rel_err(x, xref) <= 1e-10 and oracle.residual(a, b, c, d, x) <= 1e-12
+        else:
+            _check32(run(sys32, dt), *sys32)
+    for h in handles[1:]:
+        h.close()

@@ -90,3 +90,43 @@ def test_checkers():
     xr = oracle.dgtsv(a, b, c, d)
     assert oracle.residual(a, b, c, d, xr) < 1e-15
     assert oracle.residual(a, b, c, d, np.zeros(1000)) == pytest.approx(1.0)
+
+
+@pytest.mark.parametrize("n,row0,count", [(1000, 0, 1000), (1000, 999, 1), (123_457, 40_000, 50_001)])
+def test_generate_range_is_a_slice(n, row0, count):
+    full = oracle.generate(n, 9)
+    for x, y in zip(oracle.generate_range(n, row0, count, 9), full):
+        assert np.array_equal(x, y[row0:row0 + count])
+
+
+@pytest.mark.parametrize("n,chunk", [(1, 1 << 18), (5, 2), (2_000_003, 100_000), (300_000, 4096)])
+def test_windowed_check_equals_whole_system_thomas(n, chunk):
+    """orc_check_generated (windowed Thomas, pad 1024) reproduces the
+    whole-system Thomas solution bit for bit on the generated systems, so a
+    solution checked by windows is checked against Thomas itself."""
+    a, b, c, d = oracle.generate(n, 11)
+    x = oracle.thomas(a, b, c, d)
+    r = oracle.check_generated(x, n, 0, 11, chunk=chunk)
+    assert r["max_err"] == 0.0
+    assert abs(r["residual"] - oracle.residual(a, b, c, d, x)) <= 1e-3 * r["residual"] + 1e-30
+    # a slice with its halo values, and a perturbation is seen by both bars
+    lo, hi = n // 3, max(n // 3 + 1, 2 * n // 3)
+    xl = x[lo - 1] if lo > 0 else 0.0
+    xr = x[hi] if hi < n else 0.0
+    assert oracle.check_generated(x[lo:hi], n, lo, 11, xl, xr, chunk=chunk)["max_err"] == 0.0
+    xp = x.copy()
+    xp[n // 2] += 1e-7
+    rp = oracle.check_generated(xp, n, 0, 11, chunk=chunk)
+    assert rp["rel_err"] > 1e-8 and rp["residual"] > 1e-13
+
+
+def test_windowed_check_combines_over_ranks():
+    n = 1_000_000
+    a, b, c, d = oracle.generate(n, 12)
+    x = oracle.thomas(a, b, c, d)
+    cuts = [0, 250_000, 600_010, n]
+    parts = [oracle.check_generated(x[lo:hi], n, lo, 12, x[lo - 1] if lo else 0.0, x[hi] if hi < n else 0.0)
+             for lo, hi in zip(cuts[:-1], cuts[1:])]
+    r = oracle.finish_check(parts)
+    assert r["rel_err"] == 0.0
+    assert abs(r["residual"] - oracle.residual(a, b, c, d, x)) <= 1e-3 * r["residual"]
