@@ -184,9 +184,9 @@ class DistributedSolver:
     def solve(self, a, b, c, d, x, m: int = 10, stream=None):
         if self.exchange == "p2p":
             self.solver.dist_reduce_p2p(a, b, c, d, m, stream=stream)
-            k = self.solver.last_launch_count
+            k = getattr(self.solver, "last_launch_count", 0)
             self.solver.dist_solve_p2p(a, b, c, d, x, m, stream=stream)
-            self.last_launches = k + self.solver.last_launch_count
+            self.last_launches = k + getattr(self.solver, "last_launch_count", 0)
             return x
         if self.iface.dtype != b.dtype:  # FP32 solve: interface equations in FP32
             self.iface = self.iface.to(b.dtype)
@@ -204,9 +204,9 @@ class DistributedSolver:
                else contextlib.nullcontext())
         with ctx:
             self.solver.dist_reduce(a, b, c, d, m, self.rank, self.world, self.iface, stream=stream)
-            k = self.solver.last_launch_count
+            k = getattr(self.solver, "last_launch_count", 0)
             self._all_gather()
             self.solver.dist_solve(a, b, c, d, x, m, self.rank, self.world, self.iface_all, stream=stream)
         # the solver's own kernels (the all-gather's NCCL kernel is not counted)
-        self.last_launches = k + self.solver.last_launch_count
+        self.last_launches = k + getattr(self.solver, "last_launch_count", 0)
         return x
