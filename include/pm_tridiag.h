@@ -223,6 +223,50 @@ int pm_dist_solve_f64(pm_handle_t h, const double* a, const double* b, const dou
                       const double* d, double* x, int64_t n_local, int32_t m, int32_t rank,
                       int32_t world, const double* iface_all, void* stream);
 
+/* One-call collective solve of a row-sharded system (every rank calls it
+ * with its rows; BASELINE.json config 5, SURVEY.md §8b pm_solve_dist_f64):
+ * Stage 1 + local levels -> the rank's 8 interface reals, the all-gather of
+ * those 8 reals over the ranks, the 2*world-row interface solve + Stage 3 of
+ * every local level -> x.  Stream-ordered on `stream`; pivot failures are
+ * reported by pm_check.  Same row split rules as pm_dist_*: every rank but
+ * the last holds a multiple of m rows.
+ *
+ * The exchange is the caller's:
+ *   pm_solve_dist_*       `allgather(send, recv, bytes_per_rank, stream, user)`
+ *                         must gather bytes_per_rank (64 FP64 / 32 FP32) from
+ *                         every rank's device buffer `send` into `recv` in
+ *                         rank order, ordered after the work already on
+ *                         `stream` and before anything enqueued on it later
+ *                         (e.g. ncclAllGather / MPI_Allgather of a staged copy);
+ *                         non-zero return -> PM_ERR_RUNTIME.
+ *   pm_solve_dist_nccl_*  NCCL's ncclAllGather on `nccl_comm` (an ncclComm_t;
+ *                         rank and world are the communicator's).  NCCL is
+ *                         loaded at run time (PM_NCCL_LIB, else libnccl.so.2:
+ *                         the copy already in the process if any); the library
+ *                         does not link it.
+ * pm_nccl_* create a communicator without including nccl.h:
+ * pm_nccl_get_unique_id on one rank (PM_NCCL_ID_BYTES bytes, sent to the
+ * others by any side channel), pm_nccl_comm_init on every rank (on the
+ * handle's device).  pm_nccl_version: NCCL_VERSION_CODE, -1 if unloadable. */
+typedef int (*pm_allgather_fn)(const void* send, void* recv, int64_t bytes_per_rank, void* stream,
+                               void* user);
+int pm_solve_dist_f64(pm_handle_t h, const double* a, const double* b, const double* c, const double* d,
+                      double* x, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                      pm_allgather_fn allgather, void* user, void* stream);
+int pm_solve_dist_f32(pm_handle_t h, const float* a, const float* b, const float* c, const float* d,
+                      float* x, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                      pm_allgather_fn allgather, void* user, void* stream);
+int pm_solve_dist_nccl_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                           const double* d, double* x, int64_t n_local, int32_t m, void* nccl_comm,
+                           void* stream);
+int pm_solve_dist_nccl_f32(pm_handle_t h, const float* a, const float* b, const float* c, const float* d,
+                           float* x, int64_t n_local, int32_t m, void* nccl_comm, void* stream);
+#define PM_NCCL_ID_BYTES 128
+int pm_nccl_version(void);
+int pm_nccl_get_unique_id(pm_handle_t h, void* id_out);
+int pm_nccl_comm_init(pm_handle_t h, void** comm_out, int32_t world, const void* id, int32_t rank);
+int pm_nccl_comm_destroy(pm_handle_t h, void* comm);
+
 /* Peer-memory (NVLink P2P) exchange of the interface equations -- the
  * all-gather of pm_dist_* done by the solver's own kernels.  Each rank
  * allocates an exchange buffer (pm_dist_exchange_alloc; owned by the handle),

@@ -31,6 +31,9 @@ class ModelBundleC(C.Structure):
 # (name, restype, argtypes) of every symbol include/pm_tridiag.h and
 # include/streamtune_c.h declare; tests check the library exports all of them.
 _ERR = [C.c_char_p, C.c_int]
+# int allgather(const void* send, void* recv, int64_t bytes_per_rank, void* stream, void* user)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
 PM_SIGNATURES = [
     ("pm_create", C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     ("pm_destroy", C.c_int, [C.c_void_p]),
@@ -85,6 +88,18 @@ PM_SIGNATURES = [
     ("pm_dist_solve_p2p_f64", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
     ("pm_dist_reduce_p2p_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
     ("pm_dist_solve_p2p_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p]),
+    ("pm_solve_dist_f64", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32,
+                                    C.c_int32, ALLGATHER_FN, C.c_void_p, C.c_void_p]),
+    ("pm_solve_dist_f32", C.c_int, [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_int32,
+                                    C.c_int32, ALLGATHER_FN, C.c_void_p, C.c_void_p]),
+    ("pm_solve_dist_nccl_f64", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("pm_solve_dist_nccl_f32", C.c_int,
+     [C.c_void_p, _CD, _CD, _CD, _CD, _CD, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("pm_nccl_version", C.c_int, []),
+    ("pm_nccl_get_unique_id", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("pm_nccl_comm_init", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_int32]),
+    ("pm_nccl_comm_destroy", C.c_int, [C.c_void_p, C.c_void_p]),
     ("pm_last_launch_count", C.c_int, [C.c_void_p]),
     ("pm_kernel_times", C.c_int,
      [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int32]),

@@ -29,6 +29,7 @@
 
 #include "pm_batch.h"
 #include "pm_kernels.h"
+#include "pm_nccl.h"
 #include "pm_tridiag.h"
 #include "streamtune/predictor.hpp"
 
@@ -196,6 +197,8 @@ struct pm_handle_s {
   int xworld = 0, xrank = -1;
   uint64_t epoch = 0;
   void* iface_local = nullptr;
+  void* coll_buf = nullptr;  // pm_solve_dist_*: [8 | 8*world] reals (iface, iface_all)
+  size_t coll_bytes = 0;
   // set while a pm_dist_*_p2p call enqueues its top level: that launch
   // publishes (REDUCE) or acquires and chains (SOLVE) the interface rows itself
   struct P2PTop {
@@ -1248,6 +1251,68 @@ int dist_solve_p2p_impl(pm_handle_t h, const R* a, const R* b, const R* c, const
                             h->epoch);
 }
 
+// ---- one-call collective solve (pm_solve_dist_*): reduce, exchange, solve --
+// The exchange is the caller's all-gather (callback) or NCCL's (dlopen).
+// Both halves and the exchange are ordered on `stream`; the handle's
+// coll_buf holds this rank's 8 interface reals and the gathered 8*world.
+template <class R, class Gather>
+int solve_dist_impl(pm_handle_t h, const R* a, const R* b, const R* c, const R* d, R* x, int64_t n_local,
+                    int32_t m, int32_t rank, int32_t world, void* stream, Gather&& gather) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (world < 1 || rank < 0 || rank >= world) return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  const size_t need = (size_t)(8 + 8 * (size_t)world) * sizeof(R);
+  if (h->coll_bytes < need) {
+    PM_CUDA(h, cudaSetDevice(h->device));
+    if (h->coll_buf) {
+      PM_CUDA(h, cudaDeviceSynchronize());  // an earlier solve may still read it
+      cudaFree(h->coll_buf);
+      h->coll_buf = nullptr;
+      h->coll_bytes = 0;
+    }
+    PM_CUDA(h, cudaMalloc(&h->coll_buf, need));
+    h->coll_bytes = need;
+  }
+  R* iface = static_cast<R*>(h->coll_buf);
+  R* iface_all = iface + 8;
+  int r = dist_reduce_impl<R>(h, a, b, c, d, n_local, m, rank, world, iface, stream);
+  if (r) return r;
+  const int reduce_launches = h->launches;
+  std::string why;
+  if (gather(static_cast<const void*>(iface), static_cast<void*>(iface_all), why) != 0)
+    return fail(h, PM_ERR_RUNTIME, why);
+  r = dist_solve_impl<R>(h, a, b, c, d, x, n_local, m, rank, world, iface_all, stream);
+  h->launches += reduce_launches;
+  return r;
+}
+
+template <class R>
+int solve_dist_cb_impl(pm_handle_t h, const R* a, const R* b, const R* c, const R* d, R* x, int64_t n_local,
+                       int32_t m, int32_t rank, int32_t world, pm_allgather_fn allgather, void* user,
+                       void* stream) {
+  if (h && !allgather) return fail(h, PM_ERR_VALIDATION, "null all-gather callback");
+  return solve_dist_impl<R>(h, a, b, c, d, x, n_local, m, rank, world, stream,
+                            [&](const void* send, void* recv, std::string& why) {
+                              const int st = allgather(send, recv, (int64_t)(8 * sizeof(R)), stream, user);
+                              if (st != 0) why = "all-gather callback returned " + std::to_string(st);
+                              return st;
+                            });
+}
+
+template <class R>
+int solve_dist_nccl_impl(pm_handle_t h, const R* a, const R* b, const R* c, const R* d, R* x,
+                         int64_t n_local, int32_t m, void* comm, void* stream) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (!comm) return fail(h, PM_ERR_VALIDATION, "null NCCL communicator");
+  std::string why;
+  int world = 0, rank = 0;
+  if (pmnccl::comm_count(comm, &world, &why) != 0 || pmnccl::comm_user_rank(comm, &rank, &why) != 0)
+    return fail(h, PM_ERR_RUNTIME, why);
+  return solve_dist_impl<R>(h, a, b, c, d, x, n_local, m, rank, world, stream,
+                            [&](const void* send, void* recv, std::string& w) {
+                              return pmnccl::all_gather(send, recv, 8, sizeof(R) == 8, comm, stream, &w);
+                            });
+}
+
 extern "C" {
 
 int pm_get_version(void) { return 100; }
@@ -1286,6 +1351,7 @@ int pm_destroy(pm_handle_t h) {
   if (h->xbuf) cudaFree(h->xbuf);
   if (h->d_peers) cudaFree(h->d_peers);
   if (h->iface_local) cudaFree(h->iface_local);
+  if (h->coll_buf) cudaFree(h->coll_buf);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   delete h;
   return PM_OK;
@@ -1553,6 +1619,55 @@ int pm_solve_batch_host_f32(pm_handle_t h, const float* a, const float* b, const
                             const float* d, float* x, int64_t n_per_system, int64_t batch, int32_t m,
                             int32_t depth, int64_t systems_per_chunk) {
   return solve_batch_host_impl<float>(h, a, b, c, d, x, n_per_system, batch, m, depth, systems_per_chunk);
+}
+
+int pm_solve_dist_f64(pm_handle_t h, const double* a, const double* b, const double* c, const double* d,
+                      double* x, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                      pm_allgather_fn allgather, void* user, void* stream) {
+  return solve_dist_cb_impl<double>(h, a, b, c, d, x, n_local, m, rank, world, allgather, user, stream);
+}
+int pm_solve_dist_f32(pm_handle_t h, const float* a, const float* b, const float* c, const float* d,
+                      float* x, int64_t n_local, int32_t m, int32_t rank, int32_t world,
+                      pm_allgather_fn allgather, void* user, void* stream) {
+  return solve_dist_cb_impl<float>(h, a, b, c, d, x, n_local, m, rank, world, allgather, user, stream);
+}
+int pm_solve_dist_nccl_f64(pm_handle_t h, const double* a, const double* b, const double* c,
+                           const double* d, double* x, int64_t n_local, int32_t m, void* nccl_comm,
+                           void* stream) {
+  return solve_dist_nccl_impl<double>(h, a, b, c, d, x, n_local, m, nccl_comm, stream);
+}
+int pm_solve_dist_nccl_f32(pm_handle_t h, const float* a, const float* b, const float* c, const float* d,
+                           float* x, int64_t n_local, int32_t m, void* nccl_comm, void* stream) {
+  return solve_dist_nccl_impl<float>(h, a, b, c, d, x, n_local, m, nccl_comm, stream);
+}
+
+int pm_nccl_version(void) { return pmnccl::load(nullptr) ? pmnccl::version() : -1; }
+
+int pm_nccl_get_unique_id(pm_handle_t h, void* id_out) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (!id_out) return fail(h, PM_ERR_VALIDATION, "null id buffer");
+  std::string why;
+  if (pmnccl::get_unique_id(id_out, &why) != 0) return fail(h, PM_ERR_RUNTIME, why);
+  return PM_OK;
+}
+
+int pm_nccl_comm_init(pm_handle_t h, void** comm_out, int32_t world, const void* id, int32_t rank) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (!comm_out || !id) return fail(h, PM_ERR_VALIDATION, "null communicator / id pointer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(h, PM_ERR_VALIDATION, "rank must lie in [0, world)");
+  PM_CUDA(h, cudaSetDevice(h->device));
+  std::string why;
+  if (pmnccl::comm_init_rank(comm_out, world, id, rank, &why) != 0) return fail(h, PM_ERR_RUNTIME, why);
+  return PM_OK;
+}
+
+int pm_nccl_comm_destroy(pm_handle_t h, void* comm) {
+  if (!h) return PM_ERR_VALIDATION;
+  if (!comm) return PM_OK;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  std::string why;
+  if (pmnccl::comm_destroy(comm, &why) != 0) return fail(h, PM_ERR_RUNTIME, why);
+  return PM_OK;
 }
 
 int64_t pm_dist_exchange_bytes(int32_t world) {

@@ -306,6 +306,48 @@ class PartitionSolver:
         self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt),
                     self._ptr(x, n, dt), n, m, _stream_handle(stream)))
 
+    # -- one-call collective solve with the caller's exchange (C ABI) -----------
+    def solve_dist(self, a, b, c, d, x, m: int, rank: int, world: int, allgather, stream=None):
+        """pm_solve_dist_f64 / _f32: reduce -> allgather(send_ptr, recv_ptr,
+        bytes_per_rank, stream_ptr) -> solve, every rank collectively.
+        `allgather` is a Python callable returning 0 on success; it runs on
+        this thread inside the call (the GIL is released around the C call, so
+        ranks may be threads)."""
+        n, dt = int(b.numel()), b.dtype
+        fn = getattr(self._L, "pm_solve_dist_" + _suffix(dt))
+
+        def tramp(send, recv, nbytes, st, _user):
+            try:
+                return int(allgather(send, recv, nbytes, st) or 0)
+            except Exception:  # never unwind through C
+                return 1
+
+        cb = _lib.ALLGATHER_FN(tramp)
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt),
+                    self._ptr(x, n, dt), n, m, rank, world, cb, None, _stream_handle(stream)))
+        return x
+
+    def solve_dist_nccl(self, a, b, c, d, x, m: int, comm: int, stream=None):
+        """pm_solve_dist_nccl_f64 / _f32 on an ncclComm_t (see nccl_comm_init)."""
+        n, dt = int(b.numel()), b.dtype
+        fn = getattr(self._L, "pm_solve_dist_nccl_" + _suffix(dt))
+        self._ok(fn(self._h, self._ptr(a, n, dt), self._ptr(b, n, dt), self._ptr(c, n, dt), self._ptr(d, n, dt),
+                    self._ptr(x, n, dt), n, m, C.c_void_p(comm), _stream_handle(stream)))
+        return x
+
+    def nccl_get_unique_id(self) -> bytes:
+        buf = C.create_string_buffer(128)
+        self._ok(self._L.pm_nccl_get_unique_id(self._h, buf))
+        return buf.raw
+
+    def nccl_comm_init(self, world: int, uid: bytes, rank: int) -> int:
+        comm = C.c_void_p()
+        self._ok(self._L.pm_nccl_comm_init(self._h, C.byref(comm), int(world), C.c_char_p(bytes(uid)), int(rank)))
+        return int(comm.value)
+
+    def nccl_comm_destroy(self, comm: int):
+        self._ok(self._L.pm_nccl_comm_destroy(self._h, C.c_void_p(comm)))
+
     # -- stream-count model -------------------------------------------------------
     def set_model_bundle(self, bundle: "ModelBundleC"):
         self._ok(self._L.pm_set_model_bundle(self._h, C.byref(bundle)))

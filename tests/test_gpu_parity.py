@@ -485,6 +485,111 @@ def test_dist_p2p_virtual_ranks(solver, world, n, m):
         h.close()
 
 
+def _cudart():
+    import ctypes as C
+    import glob
+
+    for cand in ["/usr/local/cuda/lib64/libcudart.so", "libcudart.so.12", "libcudart.so"] + sorted(
+            glob.glob("/usr/local/cuda*/lib64/libcudart.so*")):
+        try:
+            return C.CDLL(cand)
+        except OSError:
+            continue
+    pytest.skip("libcudart not loadable")
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_solve_dist_callback_threads(solver, world, dtype):
+    """pm_solve_dist_* (one C call per rank: reduce, the caller's all-gather,
+    solve) with `world` threads as ranks on one GPU, each with its own handle
+    and stream; the all-gather callback stages the 8 interface reals through
+    host memory with a barrier, as an MPI caller would."""
+    import ctypes as C
+    import threading
+
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.dist import split_rows
+
+    cudart = _cudart()
+    n, m = 600_007, 10
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    ah, bh, ch, dh = oracle.generate(n, 29)
+    if dtype == "f32":
+        ah, bh, ch, dh = (v.astype(np.float32).astype(np.float64) for v in (ah, bh, ch, dh))
+    rows = split_rows(n, world, m)
+    offs = np.concatenate([[0], np.cumsum(rows)])
+    handles = [PartitionSolver(0) for _ in range(world)]
+    slots = torch.zeros(8 * world, dtype=tdt).pin_memory()
+    bar = threading.Barrier(world)
+    xs = [None] * world
+    errs = []
+
+    def rank_main(r):
+        try:
+            st = torch.cuda.Stream()
+            loc = [torch.from_numpy(np.ascontiguousarray(v[offs[r]:offs[r + 1]])).to(tdt).cuda() for v in
+                   (ah, bh, ch, dh)]
+            x = torch.empty(rows[r], dtype=tdt, device="cuda")
+
+            def allgather(send, recv, nbytes, stream_ptr):
+                base = slots.data_ptr()
+                ok = cudart.cudaMemcpyAsync(C.c_void_p(base + r * nbytes), C.c_void_p(send), C.c_size_t(nbytes),
+                                            4, C.c_void_p(stream_ptr)) == 0
+                ok &= cudart.cudaStreamSynchronize(C.c_void_p(stream_ptr)) == 0
+                bar.wait()  # every rank's 8 reals are in the host slots
+                ok &= cudart.cudaMemcpyAsync(C.c_void_p(recv), C.c_void_p(base), C.c_size_t(nbytes * world), 4,
+                                             C.c_void_p(stream_ptr)) == 0
+                ok &= cudart.cudaStreamSynchronize(C.c_void_p(stream_ptr)) == 0
+                bar.wait()  # nobody rewrites the slots before everyone read them
+                return 0 if ok else 1
+
+            for _ in range(2):
+                handles[r].solve_dist(*loc, x, m=m, rank=r, world=world, allgather=allgather, stream=st)
+            handles[r].check()
+            xs[r] = x.double().cpu().numpy()
+        except Exception as e:  # surfaced below
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for h in handles:
+        h.close()
+    assert not errs, errs
+    x = np.concatenate(xs)
+    if dtype == "f64":
+        _check(x, ah, bh, ch, dh)
+    else:
+        xref = oracle.thomas(ah, bh, ch, dh)
+        assert oracle.rel_err(x, xref) <= 1e-5 and oracle.residual(ah, bh, ch, dh, x) <= 1e-5
+
+
+def test_solve_dist_nccl_one_rank(solver):
+    """pm_solve_dist_nccl_f64 on a one-rank NCCL communicator created through
+    pm_nccl_* (the library dlopens NCCL; here PyTorch's copy is already loaded)."""
+    import torch
+
+    if solver._L.pm_nccl_version() < 0:
+        pytest.skip("NCCL not loadable")
+    n = 1_000_003
+    a, b, c, d = _device_system(solver, n, seed=3)
+    comm = solver.nccl_comm_init(1, solver.nccl_get_unique_id(), 0)
+    try:
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        solver.solve_dist_nccl(a, b, c, d, x, m=10, comm=comm)
+        solver.check()
+        assert solver.last_launch_count >= 3
+    finally:
+        solver.nccl_comm_destroy(comm)
+    _check(x.cpu().numpy(), *oracle.generate(n, 3))
+
+
 def test_dist_p2p_timeout_is_runtime_error(solver):
     """A peer that never publishes: the wait gives up (20 s) with PM_ERR_RUNTIME."""
     import torch
