@@ -40,8 +40,10 @@ struct BundleFit {
   FitReport sum, small, big;
   FitMetricsDoc metrics() const;
 };
+// anchored = true: the overhead forms are fitted with
+// fit_overhead_*_anchored (B200 re-fit; regression.hpp).
 BundleFit fit_bundle(const StageTimingsTable& stage, const StreamedRunTable& runs,
-                     std::uint64_t size_threshold = 1000000, std::uint64_t seed = 42);
+                     std::uint64_t size_threshold = 1000000, std::uint64_t seed = 42, bool anchored = false);
 
 // Throws ValidationError on malformed documents (missing key, non-numeric
 // coefficient, invalid candidate list).

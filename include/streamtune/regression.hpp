@@ -69,4 +69,14 @@ FitReport fit_overhead_small(const std::vector<OverheadRow>& rows, const SplitCo
 // features [N*(4/3)log2 n, (4/3)log2 n, 1]
 FitReport fit_overhead_big(const std::vector<OverheadRow>& rows, const SplitConfig& cfg);
 
+// B200 addition (not in the SPEC, whose fits are plain OLS): the same two
+// forms constrained so that T_overhead(N, n = 1) = 0 and every coefficient is
+// >= 0 -- small: a = c = 0, b >= 0; big: c = 0, a, b >= 0 (exhaustive
+// active-set least squares).  On B200 the overlappable work is ~1 % of the
+// transfers and per-stream costs are tens of microseconds, so unconstrained
+// OLS fits a negative overhead at n = 2 and predicts streaming everywhere
+// (DESIGN.md §5).  Same split, seed and metrics as the OLS fits.
+FitReport fit_overhead_small_anchored(const std::vector<OverheadRow>& rows, const SplitConfig& cfg);
+FitReport fit_overhead_big_anchored(const std::vector<OverheadRow>& rows, const SplitConfig& cfg);
+
 }  // namespace streamtune

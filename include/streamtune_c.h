@@ -73,6 +73,10 @@ int st_derive_overhead_rows(const char* stage_csv, const char* runs_csv, uint64_
  * metrics[18] = sum/small/big x train/test x {r2, mse, rmse}. */
 int st_fit_bundle(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
                   uint64_t seed, pm_model_bundle* out, double* metrics, char* err, int errlen);
+/* The same with the anchored overhead fits (T_overhead(N, 1) = 0, coefficients
+ * >= 0; streamtune::fit_overhead_*_anchored) -- the B200 re-fit. */
+int st_fit_bundle_anchored(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
+                           uint64_t seed, pm_model_bundle* out, double* metrics, char* err, int errlen);
 
 /* simulator.  stages[7] = {stage1 h2d, comp, d2h, cpu (Stage 2),
  * stage3 h2d, comp, d2h} in ms; n a valid stream count; out[3] = {total, stage-1

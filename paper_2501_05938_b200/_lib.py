@@ -136,6 +136,8 @@ PM_SIGNATURES = [
       C.POINTER(C.c_int)] + _ERR),
     ("st_fit_bundle", C.c_int,
      [C.c_char_p, C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(ModelBundleC), _D] + _ERR),
+    ("st_fit_bundle_anchored", C.c_int,
+     [C.c_char_p, C.c_char_p, C.c_uint64, C.c_uint64, C.POINTER(ModelBundleC), _D] + _ERR),
     ("st_simulate", C.c_int,
      [_D, C.c_int, C.c_double, C.c_int, _D, _D, C.c_int, C.POINTER(C.c_int)] + _ERR),
     ("st_verify_lower_bound", C.c_int,

@@ -1,7 +1,8 @@
 // streamtune_cli.cpp -- the `streamtune` command-line front end
 // (module "cli").
 //
-//   streamtune fit --stage-csv F --runs-csv F [--seed 42] [--size-threshold 1000000] --out M
+//   streamtune fit --stage-csv F --runs-csv F [--seed 42] [--size-threshold 1000000]
+//                  [--overhead-fit ols|anchored] --out M
 //   streamtune predict --model M|paper|b200 --sizes N[,N...] [--precision fp64|fp32]
 //   streamtune baseline --stage-csv F --tau T [--model M]
 //   streamtune simulate --h2d1 . --comp1 . --d2h1 . --cpu . --h2d3 . --comp3 . --d2h3 .
@@ -133,7 +134,9 @@ int cmd_fit(const Flags& f) {
   std::istringstream s1(read_file(f.need("stage-csv"))), s2(read_file(f.need("runs-csv")));
   const StageTimingsTable st = load_stage_timings(s1);
   const StreamedRunTable rt = load_streamed_runs(s2);
-  BundleFit fit = fit_bundle(st, rt, f.u64("size-threshold", 1000000), f.u64("seed", 42));
+  const std::string mode = f.get("overhead-fit", "ols");
+  if (mode != "ols" && mode != "anchored") throw ValidationError("--overhead-fit must be ols or anchored");
+  BundleFit fit = fit_bundle(st, rt, f.u64("size-threshold", 1000000), f.u64("seed", 42), mode == "anchored");
   fit.bundle.fitted_on = f.get("fitted-on", f.need("stage-csv"));
   const FitMetricsDoc met = fit.metrics();
   const std::string doc = bundle_to_document(fit.bundle, &met);

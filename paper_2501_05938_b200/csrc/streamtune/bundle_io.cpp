@@ -260,7 +260,7 @@ ModelBundle bundle_from_document(const std::string& doc) {
 }
 
 BundleFit fit_bundle(const StageTimingsTable& stage, const StreamedRunTable& runs,
-                     std::uint64_t size_threshold, std::uint64_t seed) {
+                     std::uint64_t size_threshold, std::uint64_t seed, bool anchored) {
   SplitConfig cfg;
   cfg.seed = seed;
   std::vector<std::pair<std::uint64_t, double>> sum_rows;
@@ -270,8 +270,8 @@ BundleFit fit_bundle(const StageTimingsTable& stage, const StreamedRunTable& run
   if (ovh.empty()) throw TooFewObservationsError("no overhead observations (only n = 1 runs)");
   BundleFit f;
   f.sum = fit_sum_model(sum_rows, cfg);
-  f.small = fit_overhead_small(small, cfg);
-  f.big = fit_overhead_big(big, cfg);
+  f.small = anchored ? fit_overhead_small_anchored(small, cfg) : fit_overhead_small(small, cfg);
+  f.big = anchored ? fit_overhead_big_anchored(big, cfg) : fit_overhead_big(big, cfg);
   ModelBundle& b = f.bundle;
   b.sum_a = f.sum.coefficients[0];
   b.sum_b = f.sum.coefficients[1];

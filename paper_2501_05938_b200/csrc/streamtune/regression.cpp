@@ -66,6 +66,85 @@ FitReport fit_with_split(const std::vector<Observation>& data, const SplitConfig
   return rep;
 }
 
+// Least squares with every coefficient >= 0 and only the features in
+// `allowed` free (the others fixed at 0): the minimum over the feasible
+// subsets of the allowed features (<= 3 of them here, so exhaustive).
+std::vector<double> fit_nonneg_subset(const std::vector<Observation>& obs, const std::vector<std::size_t>& allowed,
+                                      std::size_t p) {
+  std::vector<double> best(p, 0.0);
+  double best_ss = 0.0;
+  for (const Observation& o : obs) best_ss += o.target * o.target;  // the all-zero model
+  const std::size_t k = allowed.size();
+  for (std::size_t mask = 1; mask < (std::size_t{1} << k); ++mask) {
+    std::vector<std::size_t> cols;
+    for (std::size_t j = 0; j < k; ++j)
+      if (mask & (std::size_t{1} << j)) cols.push_back(allowed[j]);
+    std::vector<Observation> sub;
+    sub.reserve(obs.size());
+    for (const Observation& o : obs) {
+      Observation q;
+      q.target = o.target;
+      for (std::size_t c : cols) q.features.push_back(o.features[c]);
+      sub.push_back(std::move(q));
+    }
+    std::vector<double> beta;
+    try {
+      beta = fit_least_squares(sub);
+    } catch (const RankDeficiencyError&) {
+      continue;
+    } catch (const TooFewObservationsError&) {
+      continue;
+    }
+    if (std::any_of(beta.begin(), beta.end(), [](double v) { return v < 0.0; })) continue;
+    double ss = 0.0;
+    for (const Observation& o : sub) {
+      double r = -o.target;
+      for (std::size_t c = 0; c < cols.size(); ++c) r += beta[c] * o.features[c];
+      ss += r * r;
+    }
+    if (ss < best_ss) {
+      best_ss = ss;
+      std::fill(best.begin(), best.end(), 0.0);
+      for (std::size_t c = 0; c < cols.size(); ++c) best[cols[c]] = beta[c];
+    }
+  }
+  return best;
+}
+
+FitReport fit_anchored_with_split(const std::vector<Observation>& data, const SplitConfig& cfg,
+                                  std::vector<std::string> names, const std::vector<std::size_t>& allowed) {
+  auto split = train_test_split(data, cfg);
+  FitReport rep;
+  rep.names = std::move(names);
+  rep.coefficients = fit_nonneg_subset(split.first, allowed, data.front().features.size());
+  rep.train = report_metrics(rep.coefficients, split.first);
+  rep.test = report_metrics(rep.coefficients, split.second);
+  rep.n_train = split.first.size();
+  rep.n_test = split.second.size();
+  rep.seed = cfg.seed;
+  return rep;
+}
+
+std::vector<Observation> small_obs(const std::vector<OverheadRow>& rows) {
+  std::vector<Observation> data;
+  for (const auto& r : rows) {
+    if (r.num_streams < 1) throw ValidationError("num_streams must be >= 1");
+    data.push_back({{static_cast<double>(r.slae_size), std::log10(static_cast<double>(r.num_streams)), 1.0},
+                    r.overhead_ms});
+  }
+  return data;
+}
+
+std::vector<Observation> big_obs(const std::vector<OverheadRow>& rows) {
+  std::vector<Observation> data;
+  for (const auto& r : rows) {
+    if (r.num_streams < 1) throw ValidationError("num_streams must be >= 1");
+    const double l = (4.0 / 3.0) * std::log2(static_cast<double>(r.num_streams));
+    data.push_back({{static_cast<double>(r.slae_size) * l, l, 1.0}, r.overhead_ms});
+  }
+  return data;
+}
+
 }  // namespace
 
 std::pair<std::vector<Observation>, std::vector<Observation>> train_test_split(
@@ -181,23 +260,23 @@ FitReport fit_sum_model(const std::vector<std::pair<std::uint64_t, double>>& row
 }
 
 FitReport fit_overhead_small(const std::vector<OverheadRow>& rows, const SplitConfig& cfg) {
-  std::vector<Observation> data;
-  for (const auto& r : rows) {
-    if (r.num_streams < 1) throw ValidationError("num_streams must be >= 1");
-    data.push_back({{static_cast<double>(r.slae_size), std::log10(static_cast<double>(r.num_streams)), 1.0},
-                    r.overhead_ms});
-  }
-  return fit_with_split(data, cfg, {"a", "b", "c"});
+  return fit_with_split(small_obs(rows), cfg, {"a", "b", "c"});
 }
 
 FitReport fit_overhead_big(const std::vector<OverheadRow>& rows, const SplitConfig& cfg) {
-  std::vector<Observation> data;
-  for (const auto& r : rows) {
-    if (r.num_streams < 1) throw ValidationError("num_streams must be >= 1");
-    const double l = (4.0 / 3.0) * std::log2(static_cast<double>(r.num_streams));
-    data.push_back({{static_cast<double>(r.slae_size) * l, l, 1.0}, r.overhead_ms});
-  }
-  return fit_with_split(data, cfg, {"a", "b", "c"});
+  return fit_with_split(big_obs(rows), cfg, {"a", "b", "c"});
+}
+
+// Anchored forms: T_overhead(N, n = 1) = 0 and never negative.  Small:
+// a·N + b·log10 n + c vanishes at n = 1 for every N only with a = c = 0, so
+// b >= 0 is fitted alone.  Big: (a·N + b)·(4/3)·log2 n + c with c = 0 and
+// a, b >= 0.
+FitReport fit_overhead_small_anchored(const std::vector<OverheadRow>& rows, const SplitConfig& cfg) {
+  return fit_anchored_with_split(small_obs(rows), cfg, {"a", "b", "c"}, {1});
+}
+
+FitReport fit_overhead_big_anchored(const std::vector<OverheadRow>& rows, const SplitConfig& cfg) {
+  return fit_anchored_with_split(big_obs(rows), cfg, {"a", "b", "c"}, {0, 1});
 }
 
 }  // namespace streamtune

@@ -270,13 +270,14 @@ void bundle_to_c(const ModelBundle& b, pm_model_bundle* out) {
   for (int k = 0; k < out->num_candidates; ++k) out->candidates[k] = b.candidates[k].value();
 }
 
-int st_fit_bundle(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
-                  uint64_t seed, pm_model_bundle* out, double* met, char* err, int errlen) {
+static int fit_bundle_c(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
+                        uint64_t seed, bool anchored, pm_model_bundle* out, double* met, char* err,
+                        int errlen) {
   return guarded(err, errlen, [&] {
     std::istringstream s1(stage_csv ? stage_csv : ""), s2(runs_csv ? runs_csv : "");
     StageTimingsTable st = load_stage_timings(s1);
     StreamedRunTable rt = load_streamed_runs(s2);
-    BundleFit f = fit_bundle(st, rt, size_threshold, seed);
+    BundleFit f = fit_bundle(st, rt, size_threshold, seed, anchored);
     bundle_to_c(f.bundle, out);
     if (met) {
       const FitReport* reps[3] = {&f.sum, &f.small, &f.big};
@@ -290,6 +291,16 @@ int st_fit_bundle(const char* stage_csv, const char* runs_csv, uint64_t size_thr
       }
     }
   });
+}
+
+int st_fit_bundle(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
+                  uint64_t seed, pm_model_bundle* out, double* met, char* err, int errlen) {
+  return fit_bundle_c(stage_csv, runs_csv, size_threshold, seed, false, out, met, err, errlen);
+}
+
+int st_fit_bundle_anchored(const char* stage_csv, const char* runs_csv, uint64_t size_threshold,
+                           uint64_t seed, pm_model_bundle* out, double* met, char* err, int errlen) {
+  return fit_bundle_c(stage_csv, runs_csv, size_threshold, seed, true, out, met, err, errlen);
 }
 
 static PipelineSpec spec_from_c(const double* stages, int n, double tau_ms, int hw_queues) {

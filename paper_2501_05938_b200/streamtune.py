@@ -262,11 +262,15 @@ def derive_overhead_rows(stage_csv: str, runs_csv: str) -> list[tuple[int, int, 
     return [(int(sz[k]), int(ns[k]), float(ov[k])) for k in range(min(n.value, cap))]
 
 
-def fit_bundle(stage_csv: str, runs_csv: str, size_threshold: int = 1_000_000, seed: int = 42):
-    """cmd_fit: returns (ModelBundle, metrics dict)."""
+def fit_bundle(stage_csv: str, runs_csv: str, size_threshold: int = 1_000_000, seed: int = 42,
+               anchored: bool = False):
+    """cmd_fit: returns (ModelBundle, metrics dict).
+    anchored=True: the B200 re-fit's constrained overhead forms
+    (T_overhead(N, 1) = 0, coefficients >= 0; st_fit_bundle_anchored)."""
     b = ModelBundleC()
     met = (C.c_double * 18)()
-    _call(_lib.load().st_fit_bundle, stage_csv.encode(), runs_csv.encode(), int(size_threshold), int(seed),
+    fn = _lib.load().st_fit_bundle_anchored if anchored else _lib.load().st_fit_bundle
+    _call(fn, stage_csv.encode(), runs_csv.encode(), int(size_threshold), int(seed),
           C.byref(b), met)
     names = ("r_squared", "mse", "rmse")
     m = {}
