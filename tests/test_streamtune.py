@@ -316,24 +316,47 @@ def test_fit_bundle_recovers_paper_coefficients():
 
 
 def test_b200_refit_bundle_matches_committed_sweep():
-    """The compiled-in B200 bundle is the fit of the committed sweep data
-    (refit/pooled/, tools/refit.py) and reproduces its validation."""
+    """The compiled-in B200 bundle is the anchored fit (T_overhead(N, 1) = 0,
+    non-negative coefficients) of the committed sweep data (refit/pooled/,
+    tools/refit.py, 30 repetitions per point), and it meets the north_star
+    bar on that sweep, recomputed here from the CSV: the predicted stream
+    count is within one power of two of the measured optimum at all 30 sizes;
+    the round-2 review also asks for >= 20/30 exact and a predicted-count
+    time within 5 % of the best one at every size."""
     import json
     from pathlib import Path
 
     root = Path(__file__).resolve().parents[1] / "refit" / "pooled"
     stage = (root / "stage_timings.csv").read_text()
     runs = (root / "streamed_runs.csv").read_text()
-    fitted, _ = st.fit_bundle(stage, runs)
+    fitted, _ = st.fit_bundle(stage, runs, anchored=True)
     b = st.ModelBundle.b200()
     for k in ("sum_a", "sum_b", "small_a", "small_b", "small_c", "big_a", "big_b", "big_c"):
         assert getattr(b, k) == pytest.approx(getattr(fitted, k), rel=1e-12, abs=1e-15), k
+    # the anchored forms: no overhead for one stream, never a negative one
+    for n in (2, 4, 8, 16, 32):
+        for size in (1_000, 5_000, 999_999, 1_000_000, 80_000_000):
+            assert st.predict_overhead(b, size, n) >= 0.0
+    by = {}
+    for line in runs.strip().splitlines()[1:]:
+        n, ns, t = line.split(",")
+        by.setdefault(int(n), {})[int(ns)] = float(t)
+    assert len(by) == 30
+    exact = within = 0
+    worst = 1.0
+    for n, times in by.items():
+        best = min(times, key=times.get)
+        pred = st.recommend(b, n).chosen
+        exact += pred == best
+        within += max(pred, best) / min(pred, best) <= 2
+        worst = max(worst, times[pred] / times[best])
+    assert within == 30
+    assert exact >= 20
+    assert worst <= 1.05
     val = json.loads((root / "validation.json").read_text())
-    assert val["sizes"] == 30
+    assert (val["sizes"], val["exact"], val["within_one_power_of_two"]) == (30, exact, within)
     for row in val["rows"]:
         assert st.recommend(b, row["slae_size"]).chosen == row["predicted"]
-    # north_star bar: predicted count within one power of two of the measured optimum
-    assert val["within_one_power_of_two"] >= 28
     from paper_2501_05938_b200 import _lib
     import ctypes as C
 
