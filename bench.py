@@ -755,14 +755,14 @@ def run_batch(args, ctx):
                              "~64 MB), median, max over ranks"}
     value = n_total * args.steps / (ms / 1e3)
     peak, peak_src = peaks()
-    if plan["cluster"]:
+    if plan["kernel"] in ("cluster", "stream"):
         bpu = 40.0
         v = [t for (md, _, t) in kt if md == 4]
         kms = sum(v) / max(1, len(v))
-        kname = ("batch_cluster_kernel: 40 B/unknown (a,b,c,d read once from HBM, x written; "
+        kname = (f"batch_{plan['kernel']}_kernel: 40 B/unknown (a,b,c,d read once from HBM, x written; "
                  "Stage-3 re-read from L2)")
         ach = bpu * n_loc / (kms / 1e3) / 1e9
-        tkey = "batch_cluster_bytes_per_launch"
+        tkey = f"batch_{plan['kernel']}_bytes_per_launch"
     else:
         bpu = 72.0
         v = [t for (md, lv, t) in kt if md == 1 and lv == 0]

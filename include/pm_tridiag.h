@@ -97,15 +97,17 @@ typedef struct pm_model_bundle {
 #define PM_OPT_ROOT_M 12       /* ROOT tile = 128 * root_m rows (default 8)        */
 #define PM_OPT_PDL 13          /* programmatic dependent launch (process-wide;
                                   default on; 0 disables it for both precisions)   */
-#define PM_OPT_BATCH_CLUSTER 14 /* 1: pm_solve_batch_device_f64 runs one thread-
-                                  block cluster per system (all stages while the
-                                  system is L2-resident: 40 B/unknown of HBM
-                                  traffic) when it applies: m in {2, 8, 10, 16},
-                                  even n_per_system > 32*m, 16-byte aligned arrays,
-                                  the CTA's tile trees fit shared memory.
-                                  0 (default): one long system through the level
-                                  kernels (72 B/unknown, faster on B200 today:
-                                  DESIGN.md §6)                                   */
+#define PM_OPT_BATCH_CLUSTER 14 /* batch kernel of pm_solve_batch_device_f64:
+                                  0: one long system through the level kernels
+                                  (72 B/unknown); 1: one thread-block cluster per
+                                  system (all stages while the system is L2-
+                                  resident); 2: the tile-stream kernel (Stage 3 a
+                                  few rounds behind Stage 1 over one stream of
+                                  warp tiles, per-system Stage 2 by control warps,
+                                  40 B/unknown).  1 and 2 apply to m in
+                                  {2, 8, 10, 16}, even n_per_system, 16-byte
+                                  aligned arrays (else the level kernels run);
+                                  DESIGN.md §6                                     */
 #define PM_OPT_BATCH_L2_MB 15  /* L2 budget for the systems in flight (default 64) */
 #define PM_OPT_BATCH_CLUSTER_SIZE 16 /* force CTAs per cluster, 1..16 (0 = plan)  */
 #define PM_OPT_BATCH_WARPS 17  /* force warps per CTA, 4..16 (0 = plan)           */
@@ -122,6 +124,15 @@ typedef struct pm_model_bundle {
                                   in one launch, one co-resident CTA per level-1
                                   tile: reduce, last CTA solves level 2, each
                                   back-solves its tile (3 launches -> 1); 0: off */
+#define PM_OPT_BATCH_LAG 25    /* tile-stream kernel: rounds Stage 3 trails Stage 1
+                                  (0 = plan, >= stages + 1)                        */
+#define PM_OPT_BATCH_DISCARD 26 /* tile-stream kernel: bit 0 discards consumed
+                                  node-ring lines from L2 instead of writing them
+                                  back; bit 1 sets L2 eviction priorities on its
+                                  bulk copies (Stage-1 reads evict_last, Stage-3
+                                  re-reads and x stores evict_first); default 3  */
+#define PM_OPT_BATCH_STATS 27  /* tile-stream kernel: accumulate clock64 wait /
+                                  work counters (pm_batch_stream_stats; off)      */
 #define PM_OPT_PAIR_TILES 19   /* level-0 pair tiles (two m-blocks per lane, 64*m
                                   rows per warp tile; m in {2, 8, 10, 16}):
                                   -1 (default) = on for FP32, off for FP64; 0; 1  */
@@ -149,6 +160,21 @@ int pm_solve_batch_device_f64(pm_handle_t h, const double* a, const double* b, c
  * warps per CTA, stages, max tiles per CTA, tiles per system, clusters}; all
  * zero when the last batch solve used the level kernels. */
 int pm_last_batch_plan(pm_handle_t h, int32_t* out6);
+/* Tile-stream kernel plan of the last batch solve: [used (0/1), compute warps
+ * per CTA, stages, lag, ring rounds, CTAs, compute warps in the grid, tiles
+ * per system]. */
+int pm_last_stream_plan(pm_handle_t h, int32_t* out8);
+/* Diagnostics of the last tile-stream launch with PM_OPT_BATCH_STATS on (SM
+ * cycles summed over warps): [0] Stage-3 flag waits, [1] waits that spun,
+ * [2] mailbox waits, [3] stage (bulk copy) waits, [4] control iterations,
+ * [5] idle ones, [6] Stage-2 cycles, [7] Stage-2 solves, [8] publish (fence +
+ * atomics) cycles, [9] compute-warp cycles, [10] control-warp cycles,
+ * [11] Stage-1 jobs, [12] Stage-3 jobs.  Synchronises the device. */
+int pm_batch_stream_stats(pm_handle_t h, uint64_t* out13);
+/* Diagnostics: the first n words of the tile-stream kernel's per-system
+ * counters (Stage-1 counts | Stage-3 counts | Stage-2 flags, batch words
+ * each, as laid out by the last launch); all zero between launches. */
+int pm_batch_stream_counters(pm_handle_t h, uint32_t* out, int64_t n);
 
 /* Batch of independent systems from host memory, end to end (config 4):
  * chunks of `systems_per_chunk` systems (0 = ~64 MB of inputs per chunk) flow

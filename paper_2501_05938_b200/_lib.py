@@ -105,6 +105,9 @@ PM_SIGNATURES = [
      [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int32]),
     ("pm_last_plan", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]),
     ("pm_last_batch_plan", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    ("pm_last_stream_plan", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    ("pm_batch_stream_stats", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    ("pm_batch_stream_counters", C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.c_int64]),
     # streamtune_c.h
     ("st_stream_count_is_valid", C.c_int, [C.c_int]),
     ("st_validate_stage_timings", C.c_int, [C.POINTER(StageTimingsC)] + _ERR),

@@ -160,6 +160,16 @@ struct pm_handle_s {
   int batch_force_warps = 0;
   int batch_force_stages = 0;
   pm::BatchPlan last_batch_plan{0, 0, 0, 0, 0, 0};
+  // tile-stream batch kernel (PM_OPT_BATCH_CLUSTER = 2)
+  int batch_lag = 0;       // PM_OPT_BATCH_LAG (0 = plan)
+  int batch_discard = 3;   // PM_OPT_BATCH_DISCARD: bit 0 discard, bit 1 L2 hints
+  char* bscr = nullptr;    // node / segment / boundary-value rings
+  size_t bscr_bytes = 0;
+  char* bcnt = nullptr;    // per-system counters and flags, zero between launches
+  size_t bcnt_bytes = 0;
+  pm::StreamPlan last_stream_plan{};
+  int batch_stats = 0;                    // PM_OPT_BATCH_STATS
+  unsigned long long* dstats = nullptr;   // [13] tile-stream diagnostics
   // device scratch for upper levels (+ dist boundary values)
   char* scratch = nullptr;  // level arrays of the current solve's precision
   size_t scratch_bytes = 0;
@@ -688,6 +698,11 @@ int read_flag(pm_handle_t h, cudaStream_t st) {
     PM_CUDA(h, cudaMemsetAsync(h->dflag, 0, sizeof(int), st));
     PM_CUDA(h, cudaStreamSynchronize(st));
     if (flag & 4) return fail(h, PM_ERR_RUNTIME, "P2P interface exchange timed out (a peer never published)");
+    if (flag & 16) {
+      // counters and flags of the tile-stream kernel are inconsistent now
+      if (h->bcnt) PM_CUDA(h, cudaMemset(h->bcnt, 0, h->bcnt_bytes));
+      return fail(h, PM_ERR_RUNTIME, "batch tile-stream kernel: a Stage-3 wait for its system timed out");
+    }
     if (flag & 8) {
       PM_CUDA(h, cudaMemset(h->dsync, 0, 8 * sizeof(unsigned long long)));
       return fail(h, PM_ERR_RUNTIME, "fused upper-level kernel: level-2 flag wait timed out");
@@ -806,8 +821,89 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
       h->retry_stream = st;
     }
   }
+  h->last_stream_plan = pm::StreamPlan{};
+  pm::StreamPlan sp{};
+  if (std::is_same<R, double>::value && batch > 1 && h->batch_cluster == 2 && !h->robust_mode && aligned16(a) &&
+      aligned16(b) && aligned16(c) && aligned16(d) && aligned16(x) &&
+      pm::plan_stream(m, n_per_system, batch, h->sm_count, h->max_ctas, h->batch_force_warps, h->batch_force_stages,
+                      h->batch_lag, &sp)) {
+    // rings (no initial state) and the per-system counters (zero between
+    // launches) live in separate allocations: the counters must never
+    // overlap a previous launch's ring data when the batch size changes
+    const size_t need = pm::stream_scratch_bytes(sp, batch);
+    if (need > h->bscr_bytes) {
+      if (h->bscr) {
+        PM_CUDA(h, cudaStreamSynchronize(st));
+        PM_CUDA(h, cudaFree(h->bscr));
+        h->bscr = nullptr;
+        h->bscr_bytes = 0;
+      }
+      PM_CUDA(h, cudaMalloc(&h->bscr, need));
+      h->bscr_bytes = need;
+    }
+    const size_t cneed = (size_t)batch * 3 * sizeof(unsigned);
+    if (cneed > h->bcnt_bytes) {
+      if (h->bcnt) {
+        PM_CUDA(h, cudaStreamSynchronize(st));
+        PM_CUDA(h, cudaFree(h->bcnt));
+        h->bcnt = nullptr;
+        h->bcnt_bytes = 0;
+      }
+      PM_CUDA(h, cudaMalloc(&h->bcnt, cneed));
+      PM_CUDA(h, cudaMemset(h->bcnt, 0, cneed));
+      h->bcnt_bytes = cneed;
+    }
+    pm::StreamArgs A;  // FP64-only, like the cluster kernel
+    A.a = reinterpret_cast<const double*>(a); A.b = reinterpret_cast<const double*>(b);
+    A.c = reinterpret_cast<const double*>(c); A.d = reinterpret_cast<const double*>(d);
+    A.x = reinterpret_cast<double*>(x);
+    A.n_sys = n_per_system;
+    A.batch = batch;
+    A.m = m;
+    A.tps = sp.tps;
+    A.nw = sp.nw;
+    A.W = sp.warps;
+    A.S = sp.stages;
+    A.L = sp.lag;
+    A.Lmax = sp.lag_max;
+    A.K = sp.ring;
+    A.mg_tps = pm::stream_magic((uint32_t)sp.tps);
+    A.mg_K = pm::stream_magic((uint32_t)sp.ring);
+    A.mg_period = pm::stream_magic((uint32_t)sp.ring * (uint32_t)sp.nw);
+    const size_t slots = (size_t)sp.ring * sp.nw;
+    A.cnt1 = reinterpret_cast<unsigned*>(h->bcnt);  // [3][batch], zero between launches
+    A.cnt3 = A.cnt1 + batch;
+    A.sflag = A.cnt3 + batch;
+    char* p = h->bscr;
+    A.nodes = reinterpret_cast<unsigned char*>(p);
+    p += slots * 1792;
+    A.segs = reinterpret_cast<double*>(p);
+    p += slots * 8 * sizeof(double);
+    A.txy = reinterpret_cast<double*>(p);
+    A.flag = h->dflag;
+    A.discard = h->batch_discard & 1;
+    A.hints = (h->batch_discard >> 1) & 1;
+    if (h->batch_stats) {
+      if (!h->dstats) PM_CUDA(h, cudaMalloc(&h->dstats, 16 * sizeof(unsigned long long)));
+      PM_CUDA(h, cudaMemsetAsync(h->dstats, 0, 16 * sizeof(unsigned long long), st));
+      A.stats = h->dstats;
+    }
+    h->levels.clear();
+    h->last_batch_plan = pm::BatchPlan{0, 0, 0, 0, 0, 0};
+    h->last_stream_plan = sp;
+    const bool timed = h->ktimes && next_kevent(h) != nullptr;
+    const size_t ev = h->krec.size() * 2;
+    if (timed) cudaEventRecord(h->kev[ev], st);
+    PM_CUDA(h, pm::launch_batch_stream(m, A, sp, st));
+    if (timed) {
+      cudaEventRecord(h->kev[ev + 1], st);
+      h->krec.push_back({4, 0, ev});
+    }
+    ++h->launches;
+    return PM_OK;
+  }
   pm::BatchPlan pl{};
-  if (std::is_same<R, double>::value && batch > 1 && h->batch_cluster && !h->robust_mode && aligned16(a) && aligned16(b) && aligned16(c) &&
+  if (std::is_same<R, double>::value && batch > 1 && h->batch_cluster == 1 && !h->robust_mode && aligned16(a) && aligned16(b) && aligned16(c) &&
       aligned16(d) && aligned16(x) &&
       pm::plan_batch(m, n_per_system, batch, h->sm_count, (int64_t)h->batch_l2_mb << 20,
                      h->batch_force_cluster, h->batch_force_warps, h->batch_force_stages, &pl)) {
@@ -1345,6 +1441,9 @@ int pm_destroy(pm_handle_t h) {
   for (cudaEvent_t e : h->kev) cudaEventDestroy(e);
   if (h->main) cudaStreamDestroy(h->main);
   if (h->scratch) cudaFree(h->scratch);
+  if (h->bscr) cudaFree(h->bscr);
+  if (h->bcnt) cudaFree(h->bcnt);
+  if (h->dstats) cudaFree(h->dstats);
   if (h->hbuf) cudaFree(h->hbuf);
   if (h->dflag) cudaFree(h->dflag);
   if (h->dsync) cudaFree(h->dsync);
@@ -1415,7 +1514,20 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       h->warps_per_cta = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_CLUSTER:
-      h->batch_cluster = value ? 1 : 0;
+      if (value < 0 || value > 2) return fail(h, PM_ERR_VALIDATION, "batch kernel must be 0, 1 or 2");
+      h->batch_cluster = (int)value;
+      return PM_OK;
+    case PM_OPT_BATCH_LAG:
+      if (value < 0 || (value & 0xff) > 64 || (value >> 8) > 65)
+        return fail(h, PM_ERR_VALIDATION, "batch lag must be L + 256 * (extra + 1), L in [0, 64], extra in [0, 64]");
+      h->batch_lag = (int)value;
+      return PM_OK;
+    case PM_OPT_BATCH_DISCARD:
+      if (value < 0 || value > 3) return fail(h, PM_ERR_VALIDATION, "batch discard must lie in [0, 3]");
+      h->batch_discard = (int)value;
+      return PM_OK;
+    case PM_OPT_BATCH_STATS:
+      h->batch_stats = value ? 1 : 0;
       return PM_OK;
     case PM_OPT_BATCH_L2_MB:
       if (value < 1 || value > 1024) return fail(h, PM_ERR_VALIDATION, "L2 budget must lie in [1, 1024] MB");
@@ -1426,8 +1538,8 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       h->batch_force_cluster = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_WARPS:
-      if (value != 0 && (value < 4 || value > 16))
-        return fail(h, PM_ERR_VALIDATION, "batch warps must be 0 or lie in [4, 16]");
+      if (value != 0 && (value < 2 || value > 16))
+        return fail(h, PM_ERR_VALIDATION, "batch warps must be 0 or lie in [2, 16]");
       h->batch_force_warps = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_STAGES:
@@ -1488,6 +1600,38 @@ int pm_last_batch_plan(pm_handle_t h, int32_t* out6) {
   const pm::BatchPlan& p = h->last_batch_plan;
   out6[0] = p.cluster; out6[1] = p.warps; out6[2] = p.stages;
   out6[3] = p.kmax; out6[4] = p.ntiles; out6[5] = p.clusters;
+  return PM_OK;
+}
+
+int pm_last_stream_plan(pm_handle_t h, int32_t* out8) {
+  if (!h || !out8) return PM_ERR_VALIDATION;
+  const pm::StreamPlan& p = h->last_stream_plan;
+  out8[0] = p.ctas > 0; out8[1] = p.warps; out8[2] = p.stages; out8[3] = p.lag;
+  out8[4] = p.ring; out8[5] = p.ctas; out8[6] = p.nw; out8[7] = p.tps;
+  return PM_OK;
+}
+
+int pm_batch_stream_stats(pm_handle_t h, uint64_t* out13) {
+  if (!h || !out13) return PM_ERR_VALIDATION;
+  if (!h->dstats) {
+    std::memset(out13, 0, 13 * sizeof(uint64_t));
+    return PM_OK;
+  }
+  PM_CUDA(h, cudaSetDevice(h->device));
+  PM_CUDA(h, cudaDeviceSynchronize());
+  PM_CUDA(h, cudaMemcpy(out13, h->dstats, 13 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return PM_OK;
+}
+
+int pm_batch_stream_counters(pm_handle_t h, uint32_t* out, int64_t n) {
+  if (!h || !out || n < 0) return PM_ERR_VALIDATION;
+  const int64_t have = (int64_t)(h->bcnt_bytes / sizeof(uint32_t));
+  std::memset(out, 0, (size_t)n * sizeof(uint32_t));
+  if (n > have) n = have;
+  if (!h->bcnt || n == 0) return PM_OK;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  PM_CUDA(h, cudaDeviceSynchronize());
+  PM_CUDA(h, cudaMemcpy(out, h->bcnt, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return PM_OK;
 }
 

@@ -35,6 +35,9 @@ PM_OPT_BATCH_L2_MB = 15
 PM_OPT_BATCH_CLUSTER_SIZE = 16
 PM_OPT_BATCH_WARPS = 17
 PM_OPT_BATCH_STAGES = 18
+PM_OPT_BATCH_LAG = 25
+PM_OPT_BATCH_DISCARD = 26
+PM_OPT_BATCH_STATS = 27
 PM_OPT_PAIR_TILES = 19
 PM_OPT_UPPER_CTA_M = 20
 PM_OPT_UPPER_CTA_P = 21
@@ -153,10 +156,26 @@ class PartitionSolver:
         return int(self._L.pm_last_launch_count(self._h))
 
     def last_batch_plan(self) -> dict:
-        """Cluster-kernel configuration of the last batch solve (zeros: level kernels)."""
+        """Batch-kernel configuration of the last batch solve: "kernel" is
+        "level", "cluster" (cluster, warps, stages, kmax, ntiles, clusters) or
+        "stream" (stream = {warps, stages, lag, ring, ctas, nw, tps})."""
         out = (C.c_int32 * 6)()
         self._L.pm_last_batch_plan(self._h, out)
-        return dict(zip(("cluster", "warps", "stages", "kmax", "ntiles", "clusters"), list(out)))
+        d = dict(zip(("cluster", "warps", "stages", "kmax", "ntiles", "clusters"), list(out)))
+        sp = (C.c_int32 * 8)()
+        self._L.pm_last_stream_plan(self._h, sp)
+        d["stream"] = dict(zip(("warps", "stages", "lag", "ring", "ctas", "nw", "tps"), list(sp)[1:])) \
+            if sp[0] else None
+        d["kernel"] = "stream" if sp[0] else ("cluster" if d["cluster"] else "level")
+        return d
+
+    def batch_stream_stats(self) -> dict:
+        """Diagnostics of the last tile-stream launch (PM_OPT_BATCH_STATS)."""
+        out = (C.c_uint64 * 13)()
+        self._ok(self._L.pm_batch_stream_stats(self._h, out))
+        keys = ("cflag_wait_cyc", "cflag_waits", "mbox_wait_cyc", "stage_wait_cyc", "ctl_iters", "ctl_idle",
+                "stage2_cyc", "stage2_n", "publish_cyc", "compute_cyc", "control_cyc", "a_jobs", "c_jobs")
+        return dict(zip(keys, [int(v) for v in out]))
 
     def last_plan(self) -> list[int]:
         buf = (C.c_int64 * 16)()

@@ -65,12 +65,13 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--single", required=True, help="launch list of bench.py (config 3)")
     p.add_argument("--batch", help="launch list of bench.py --workload batch (level kernels)")
-    p.add_argument("--batch-cluster", help="launch list of the batch cluster/stream kernel")
+    p.add_argument("--batch-cluster", help="launch list of the batch cluster kernel")
+    p.add_argument("--batch-stream", help="launch list of the batch tile-stream kernel")
     p.add_argument("--out", default=str(ROOT / "profiles" / "ncu_traffic.json"))
     a = p.parse_args()
     doc = {"build_hash": bench.kernel_build_hash(),
            "source": "tools/stamp_traffic.py from ncu launch lists (last launch of each kernel): "
-                     + ", ".join(Path(x).name for x in (a.single, a.batch, a.batch_cluster) if x)}
+                     + ", ".join(Path(x).name for x in (a.single, a.batch, a.batch_cluster, a.batch_stream) if x)}
     s = per_launch(a.single)
     doc["reduce_level0_bytes_per_launch"] = last_of(s, "warp_tile_kernel<10, 0")
     doc["solve_level0_bytes_per_launch"] = last_of(s, "warp_tile_kernel<10, 1")
@@ -80,7 +81,10 @@ def main():
         doc["batch_solve_level0_bytes_per_launch"] = last_of(b, "warp_tile_kernel<10, 1")
     if a.batch_cluster:
         c = per_launch(a.batch_cluster)
-        doc["batch_cluster_bytes_per_launch"] = last_of(c, "batch_")
+        doc["batch_cluster_bytes_per_launch"] = last_of(c, "batch_cluster")
+    if a.batch_stream:
+        c = per_launch(a.batch_stream)
+        doc["batch_stream_bytes_per_launch"] = last_of(c, "batch_stream")
     Path(a.out).write_text(json.dumps(doc, indent=1) + "\n")
     print(json.dumps(doc, indent=1))
 
