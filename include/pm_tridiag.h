@@ -169,12 +169,21 @@ int pm_last_stream_plan(pm_handle_t h, int32_t* out8);
  * [2] mailbox waits, [3] stage (bulk copy) waits, [4] control iterations,
  * [5] idle ones, [6] Stage-2 cycles, [7] Stage-2 solves, [8] publish (fence +
  * atomics) cycles, [9] compute-warp cycles, [10] control-warp cycles,
- * [11] Stage-1 jobs, [12] Stage-3 jobs.  Synchronises the device. */
-int pm_batch_stream_stats(pm_handle_t h, uint64_t* out13);
+ * [11] Stage-1 jobs, [12] Stage-3 jobs, [13] unused, [14] Stage-2 ns (start
+ * to flag, summed).  Synchronises the device. */
+int pm_batch_stream_stats(pm_handle_t h, uint64_t* out15);
 /* Diagnostics: the first n words of the tile-stream kernel's per-system
- * counters (Stage-1 counts | Stage-3 counts | Stage-2 flags, batch words
- * each, as laid out by the last launch); all zero between launches. */
+ * counters (Stage-1 counts | Stage-3 counts | Stage-2 flags, 32 * batch words
+ * each -- one 128-byte line per system -- as laid out by the last launch); all
+ * zero between launches. */
 int pm_batch_stream_counters(pm_handle_t h, uint32_t* out, int64_t n);
+/* Diagnostics (PM_OPT_BATCH_STATS): the first n words of the last tile-stream
+ * launch's trace buffer: per-system globaltimer stamps, [5][batch] words
+ * (first Stage-1 start | last Stage-1 end | Stage-1 count complete | Stage-2
+ * flag | first Stage-3 wait start), then job traces of 8 sample warps
+ * [8][2400][4] (job code, start, stage ready, end), the control warp of CTA 0
+ * [1200][2], and per-warp / per-CTA cycle summaries [4096][8]. */
+int pm_batch_stream_timeline(pm_handle_t h, uint64_t* out, int64_t n);
 
 /* Batch of independent systems from host memory, end to end (config 4):
  * chunks of `systems_per_chunk` systems (0 = ~64 MB of inputs per chunk) flow

@@ -108,6 +108,7 @@ PM_SIGNATURES = [
     ("pm_last_stream_plan", C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     ("pm_batch_stream_stats", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     ("pm_batch_stream_counters", C.c_int, [C.c_void_p, C.POINTER(C.c_uint32), C.c_int64]),
+    ("pm_batch_stream_timeline", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]),
     # streamtune_c.h
     ("st_stream_count_is_valid", C.c_int, [C.c_int]),
     ("st_validate_stage_timings", C.c_int, [C.POINTER(StageTimingsC)] + _ERR),

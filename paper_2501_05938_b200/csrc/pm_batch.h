@@ -40,6 +40,11 @@ int plan_batch(int m, int64_t n_sys, int64_t batch, int sm_count, int64_t l2_bud
 cudaError_t launch_batch_cluster(int m, const BatchArgs& args, const BatchPlan& plan, cudaStream_t st);
 
 // ---- the tile-stream kernel (pm_batch_stream.cu) ----------------------------
+// Per-system counters and flags sit kStreamCounterStride words apart (one
+// 128-byte L2 line each): ~1000 warps poll the flags of the few systems in
+// flight, and packed 32 to a line those polls, the Stage-1/Stage-3 atomics and
+// the Stage-2 releases all hit one L2 slice.
+constexpr int kStreamCounterStride = 32;
 struct StreamArgs {
   const double* a = nullptr;  // batch systems stored back to back, n_sys rows each
   const double* b = nullptr;
@@ -60,13 +65,14 @@ struct StreamArgs {
   double* segs = nullptr;          // [K*nw] tile segments (8 doubles)
   double* txy = nullptr;           // [K*nw] tile boundary values (2 doubles)
   unsigned char* nodes = nullptr;  // [K*nw] tile tree nodes (1792 B)
-  unsigned* cnt1 = nullptr;        // [batch] Stage-1 tiles published
-  unsigned* cnt3 = nullptr;        // [batch] Stage-3 tiles done
-  unsigned* sflag = nullptr;       // [batch] Stage 2 done
+  unsigned* cnt1 = nullptr;        // [batch][stride] Stage-1 tiles published
+  unsigned* cnt3 = nullptr;        // [batch][stride] Stage-3 tiles done
+  unsigned* sflag = nullptr;       // [batch][stride] Stage 2 done
   int* flag = nullptr;
   int discard = 1;  // discard.global.L2 on consumed node-ring lines
   int hints = 1;    // L2 eviction priorities on the bulk copies
-  unsigned long long* stats = nullptr;  // [13] diagnostics (PM_OPT_BATCH_STATS) or null
+  unsigned long long* stats = nullptr;  // [15] diagnostics (PM_OPT_BATCH_STATS) or null
+  unsigned long long* tl = nullptr;     // [5][batch] per-system timeline (with stats)
 };
 
 struct StreamPlan {

@@ -58,9 +58,9 @@ namespace {
 constexpr int kNodeBytes = 1792;  // 31 Nodes (1736 B) padded to 14 x 128 B
 constexpr int kNodeCopy = 1744;   // 16-byte multiple covering the 31 nodes
 constexpr int kMbox = 8;          // mailbox slots per compute warp
+constexpr int kCS = kStreamCounterStride;  // a system's counters / flag: one 128-byte line each
 constexpr int kStreamMaxWarps = 14;
 constexpr int kStreamThreads = 32 * (kStreamMaxWarps + 2);  // + control warp + Stage-2 warp
-constexpr int kQueue = 64;        // completed systems handed to the Stage-2 warp
 constexpr uint64_t kStreamWaitNs = 20ull * 1000ull * 1000ull * 1000ull;
 constexpr int kFlagTimeout = 16;  // status bit: a Stage-3 wait timed out
 
@@ -75,10 +75,8 @@ struct Layout {
   size_t mbox;    // [W][kMbox] Seg
   size_t wnode;   // 31 Node: control warp's tree
   size_t chain;   // [tps] Seg: one system's tile segments, chain nodes in place
-  size_t queue;   // [kQueue] int64 systems whose Stage-1 count completed (-1: end)
-  size_t qbar;    // [2][kQueue] mbarriers: queue slot full | empty
   size_t gbar;    // mbarrier of the Stage-2 warp's segment gather
-  size_t zbar;    // [W] never-completing mbarriers: timed sleeps of the flag wait
+  size_t zbar;    // [W + 1] never-completing mbarriers: timed sleeps of the flag waits
   size_t total;
 };
 
@@ -102,14 +100,10 @@ __host__ __device__ inline Layout stream_layout(int m, int W, int S, int tps) {
   o = align_up(o, 16);
   L.chain = o;
   o += (size_t)tps * sizeof(Seg);
-  L.queue = o;
-  o += kQueue * sizeof(long long);
-  L.qbar = o;
-  o += 2 * kQueue * sizeof(uint64_t);
   L.gbar = o;
   o += sizeof(uint64_t);
   L.zbar = o;
-  o += (size_t)W * sizeof(uint64_t);
+  o += (size_t)(W + 1) * sizeof(uint64_t);
   L.total = align_up(o, 128);
   return L;
 }
@@ -156,9 +150,12 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 // mailbox-full wait cycles, [3] stage wait cycles, [4] control iterations,
 // [5] idle control iterations, [6] Stage-2 cycles, [7] Stage-2 count,
 // [8] control publish (fence + atomics) cycles, [9] compute-warp cycles,
-// [10] control-warp cycles, [11] A jobs, [12] C jobs.
+// [10] control-warp cycles, [11] A jobs, [12] C jobs, [13] (unused), [14]
+// ns from a system's Stage-2 start to its flag.  With stats on, A.tl also
+// gets per-system globaltimer stamps, job traces of 8 sample warps and
+// per-warp / per-CTA cycle summaries (tools/stream_probe.py reads them).
 struct Stats {
-  unsigned long long v[13];
+  unsigned long long v[15];
 };
 __device__ __forceinline__ long long clk() { return clock64(); }
 
@@ -326,6 +323,14 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
   Stats st{};
   const long long t_begin = clk();
   int na = 0;  // A jobs published so far (mailbox cursor)
+  unsigned long long st_a_cyc = 0, st_c_cyc = 0, st_ai_cyc = 0, st_ci_cyc = 0;
+  // job trace of 8 sample warps (diagnostics): [code, start, stage ready, end]
+  unsigned long long* trace = nullptr;
+  if (A.tl) {
+    const int tw[8] = {0, 1, 7, 8, 300, 591, 1000, 1183};
+    for (int i = 0; i < 8; ++i)
+      if (gw == tw[i] && tw[i] < A.nw) trace = A.tl + 5 * A.batch + (size_t)i * 2400 * 4;
+  }
   for (int k = 0; k < njobs; ++k) {
     const int s = (S == 2) ? (k & 1) : 0;  // S is 1 or 2 (plan)
     const int code = __shfl_sync(0xffffffffu, s == 0 ? jq0 : jq1, 0);
@@ -333,7 +338,7 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
     const Geo g = geo_of(A, j.r, gw);
     // prefetch the flag the next issue decision may need
     if (lane == 0 && c_iss < a_iss && a_iss - c_iss >= Lmin && c_iss < R)
-      c_ready = ld_relaxed_u32(A.sflag + fdiv(static_cast<uint32_t>(c_iss) * A.nw + gw, A.mg_tps));
+      c_ready = ld_relaxed_u32(A.sflag + kCS * fdiv(static_cast<uint32_t>(c_iss) * A.nw + gw, A.mg_tps));
     double* sa = rows(s);
     double* sb = sa + T;
     double* sc = sa + 2 * T;
@@ -353,10 +358,16 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
     const int nblk = (g.valid + M - 1) / M;
 
     // the Stage-3 job's system flag first: the wait (rare) overlaps the copy
-    unsigned* cflag = A.sflag + g.sys;
+    unsigned* cflag = A.sflag + kCS * g.sys;
     double xf = 0.0, xl = 0.0;
     unsigned c_old = 0;
+    const bool tr = trace && lane == 0 && k < 2400;
+    if (tr) {
+      trace[4 * k] = (unsigned long long)code;
+      trace[4 * k + 1] = gtimer();
+    }
     if (j.solve) {
+      if (A.tl && lane == 0) atomicMin(A.tl + 4 * A.batch + g.sys, (unsigned long long)gtimer());
       // Warp-uniform wait (lane 0 polls, the result is broadcast: the loop is
       // provably convergent, so the shuffle trees below stay plain SHFL):
       // relaxed polls with sleeps, then one acquire load.
@@ -382,7 +393,7 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
         const double2 v = __ldcg(txy_ring(A) + g.slot);
         xf = v.x;
         xl = v.y;
-        c_old = atomicAdd(A.cnt3 + g.sys, 1u);  // result used at the end of the job
+        c_old = atomicAdd(A.cnt3 + kCS * g.sys, 1u);  // result used at the end of the job
       }
     }
     {
@@ -390,11 +401,14 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
       mbar_wait(&bars[s], static_cast<uint32_t>((S == 2 ? (k >> 1) : k) & 1));
       st.v[3] += clk() - c0;
     }
+    if (tr) trace[4 * k + 2] = gtimer();
+    const long long c_job = clk();
     SmemAcc sacc{sa + r0, sb + r0, sc + r0, sd + r0, nullptr};
     sacc.fixup(r0, M, ctx);
     const PairAcc<M> pa{sa + r0, sb + r0, sc + r0, sd + r0};
     ++st.v[j.solve ? 12 : 11];
 
+    if (A.tl && lane == 0 && !j.solve) atomicMin(A.tl + g.sys, (unsigned long long)gtimer());
     if (!j.solve) {
       // ---- A: Stage 1 of the tile -------------------------------------------
       const Seg seg = block_reduce_fast<M, false>(pa, bad);
@@ -411,6 +425,7 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
         st.v[2] += clk() - c0;
         mbox[q] = top;
         mbar_arrive(&mfull[q]);
+        if (A.tl) atomicMax(A.tl + 1 * A.batch + g.sys, (unsigned long long)gtimer());
       }
       ++na;
     } else {
@@ -441,21 +456,38 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
           bulk_s2g(A.x + off + ctx.row0, sb, static_cast<uint32_t>(g.valid) * sizeof(double));
         bulk_commit();
         if (c_old == static_cast<unsigned>(A.tps) - 1) {  // the system's last Stage-3 tile
-          A.cnt3[g.sys] = 0;
+          A.cnt3[kCS * g.sys] = 0;
           *cflag = 0;
         }
       }
     }
     __syncwarp();
+    const long long c_iss0 = clk();
+    (j.solve ? st_c_cyc : st_a_cyc) += c_iss0 - c_job;
     if (lane == 0 && k + S < njobs) {
       bulk_wait_read0();  // the bulk store has read the stage
       issue(s);
     }
+    if (tr) trace[4 * k + 3] = gtimer();
+    (j.solve ? st_ci_cyc : st_ai_cyc) += clk() - c_iss0;
   }
   if (lane == 0) bulk_wait0();
   st.v[9] = clk() - t_begin;
+  if (A.tl && lane == 0 && gw < 4096) {  // per-warp summary: A cycles, C cycles, C wait cycles, SM id
+    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)gw * 8;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    sm[0] = st_a_cyc;
+    sm[1] = st_c_cyc;
+    sm[2] = st.v[0];
+    sm[3] = smid;
+    sm[4] = st_ai_cyc;
+    sm[5] = st_ci_cyc;
+    sm[6] = st.v[2];
+    sm[7] = st.v[3];
+  }
   if (A.stats && lane == 0)
-    for (int i = 0; i < 13; ++i)
+    for (int i = 0; i < 15; ++i)
       if (st.v[i]) atomicAdd(A.stats + i, st.v[i]);
 }
 
@@ -520,47 +552,71 @@ __device__ __forceinline__ void system_stage2(const StreamArgs& A, uint32_t s, S
   __syncwarp();
   __threadfence();  // every lane's x values before the flag
   if (lane == 0) {
-    A.cnt1[s] = 0;  // no other Stage-1 arrival for s in this launch
-    st_release_u32(A.sflag + s, 1u);
+    A.cnt1[kCS * s] = 0;  // no other Stage-1 arrival for s in this launch
+    st_release_u32(A.sflag + kCS * s, 1u);
+    if (A.tl) A.tl[3 * A.batch + s] = gtimer();
   }
   __syncwarp();
   fence_proxy_async();  // the chain nodes written in place -> before the next gather
 }
 
-// The Stage-2 warp: solves the systems the control warp queues, in order,
-// sleeping in mbarrier waits in between (no polling).
+// The Stage-2 warp of CTA b owns systems b, b + G, b + 2G, ... (G = the
+// grid): it waits for each one's Stage-1 count in turn (timed sleeps between
+// relaxed polls, then one acquire) and solves it.  A fixed owner keeps the
+// Stage-2 work spread evenly; handing a system to whichever CTA published its
+// last tile (round-2 first version) made the slowest CTA the Stage-2 server
+// for a quarter of the batch -- a positive feedback loop that slowed that SM's
+// compute warps 6x and, through the lag bound, the whole grid (22 ms/batch).
+// In-order service cannot deadlock: Stage 1 of system s depends only on the
+// Stage 2 of systems before s (through the compute warps' lag bound).
 __device__ __forceinline__ void solver_warp(const StreamArgs& A, unsigned char* smem, const Layout& lay, int lane,
                                             bool& bad) {
-  const long long* queue = reinterpret_cast<const long long*>(smem + lay.queue);
-  uint64_t* qfull = reinterpret_cast<uint64_t*>(smem + lay.qbar);
-  uint64_t* qempty = qfull + kQueue;
   uint64_t* gbar = reinterpret_cast<uint64_t*>(smem + lay.gbar);
+  uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + lay.zbar) + A.W;
   Seg* tsegs = reinterpret_cast<Seg*>(smem + lay.chain);
   Node* wnode = reinterpret_cast<Node*>(smem + lay.wnode);
   uint32_t gphase = 0;
   Stats st{};
-  for (int head = 0;; ++head) {
-    const int q = head % kQueue;
-    mbar_wait(&qfull[q], static_cast<uint32_t>((head / kQueue) & 1));
-    const long long sys = queue[q];
+  const unsigned tps = static_cast<unsigned>(A.tps);
+  for (int64_t sys = blockIdx.x; sys < A.batch; sys += gridDim.x) {
+    const unsigned* cnt = A.cnt1 + kCS * sys;
+    unsigned ok = (lane == 0) ? (ld_relaxed_u32(cnt) == tps) : 0u;
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    if (!ok) {
+      const uint64_t t0 = gtimer();
+      while (!ok) {
+        unsigned v = sleep_on(zbar, 500);
+        v |= (lane == 0) ? (ld_relaxed_u32(cnt) == tps) : 0u;
+        if (lane == 0 && !v && gtimer() - t0 > kStreamWaitNs) {
+          atomicOr(A.flag, kFlagTimeout);
+          v = 1u;
+        }
+        ok = __shfl_sync(0xffffffffu, v, 0);
+      }
+    }
+    if (lane == 0) (void)ld_acquire_u32(cnt);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&qempty[q]);
-    if (sys < 0) break;
+    const unsigned long long tq = (A.tl && lane == 0) ? gtimer() : 0ull;
     const long long c0 = clk();
     system_stage2(A, static_cast<uint32_t>(sys), tsegs, wnode, gbar, gphase, lane, bad);
     st.v[6] += clk() - c0;
+    if (A.tl && lane == 0) st.v[14] += gtimer() - tq;
     ++st.v[7];
   }
+  if (A.tl && lane == 0 && A.W * gridDim.x + blockIdx.x < 4096) {  // per-CTA Stage-2 count and cycles
+    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)(A.W * gridDim.x + blockIdx.x) * 8;
+    sm[0] = st.v[7];
+    sm[1] = st.v[6];
+  }
   if (A.stats && lane == 0)
-    for (int i = 6; i < 8; ++i)
+    for (int i = 6; i < 15; ++i)
       if (st.v[i]) atomicAdd(A.stats + i, st.v[i]);
 }
 
 // The control warp: lane w takes compute warp w's Stage-1 segments in round
 // order (blocking mbarrier waits: the warps of a CTA advance together), stores
 // them into the segment ring, and publishes a round's segments with one fence
-// and one atomicAdd per system touched; systems whose count completes go to
-// the Stage-2 warp's queue.
+// and one atomicAdd per system touched.
 __device__ __forceinline__ void control_warp(const StreamArgs& A, unsigned char* smem, const Layout& lay, int lane,
                                              bool& bad) {
   (void)bad;
@@ -573,21 +629,12 @@ __device__ __forceinline__ void control_warp(const StreamArgs& A, unsigned char*
   uint64_t* mfull = reinterpret_cast<uint64_t*>(smem + lay.mfull) + lane * kMbox;
   uint64_t* mempty = reinterpret_cast<uint64_t*>(smem + lay.mempty) + lane * kMbox;
   const Seg* mbox = reinterpret_cast<const Seg*>(smem + lay.mbox) + lane * kMbox;
-  long long* queue = reinterpret_cast<long long*>(smem + lay.queue);
-  uint64_t* qfull = reinterpret_cast<uint64_t*>(smem + lay.qbar);
-  uint64_t* qempty = qfull + kQueue;
-  int tail = 0;
   Stats st{};
   const long long t_begin = clk();
-  auto push = [&](long long sys) {  // lane 0
-    const int q = tail % kQueue;
-    mbar_wait(&qempty[q], static_cast<uint32_t>(((tail / kQueue) & 1) ^ 1));
-    queue[q] = sys;
-    mbar_arrive(&qfull[q]);
-    ++tail;
-  };
+  unsigned long long* ctr = (A.tl && blockIdx.x == 0) ? A.tl + 5 * A.batch + 8 * 2400 * 4 : nullptr;
   for (int c = 0; c < Rmax; ++c) {
     ++st.v[4];
+    if (ctr && lane == 0 && c < 1200) ctr[2 * c] = gtimer();
     const bool active = c < R;
     long long sys = -1;
     if (active) {
@@ -602,26 +649,21 @@ __device__ __forceinline__ void control_warp(const StreamArgs& A, unsigned char*
     __syncwarp();
     __threadfence();  // release: the segments stored above, before the counts
     const unsigned grp = __match_any_sync(0xffffffffu, sys);
-    bool done = false;
     if (active && (__ffs(grp) - 1) == lane) {
       const unsigned n = __popc(grp);
-      done = (atomicAdd(A.cnt1 + sys, n) + n == static_cast<unsigned>(A.tps));
-    }
-    unsigned dm = __ballot_sync(0xffffffffu, done);
-    if (dm) {
-      __threadfence();  // acquire: every CTA's segments of the completed systems
-      while (dm) {
-        const int src = __ffs(dm) - 1;
-        dm &= dm - 1;
-        const long long s2 = __shfl_sync(0xffffffffu, sys, src);
-        if (lane == 0) push(s2);
-      }
+      const unsigned old = atomicAdd(A.cnt1 + kCS * sys, n);
+      if (A.tl && old + n == static_cast<unsigned>(A.tps)) A.tl[2 * A.batch + sys] = gtimer();
     }
     __syncwarp();
     st.v[8] += clk() - c0;
+    if (ctr && lane == 0 && c < 1200) ctr[2 * c + 1] = gtimer();
   }
-  if (lane == 0) push(-1);  // end of the queue
   st.v[10] = clk() - t_begin;
+  if (A.tl && lane == 0 && A.W * gridDim.x + blockIdx.x < 4096) {
+    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)(A.W * gridDim.x + blockIdx.x) * 8;
+    sm[2] = st.v[8];
+    sm[3] = st.v[10];
+  }
   if (A.stats && lane == 0)
     for (int i = 0; i < 13; ++i)
       if (st.v[i]) atomicAdd(A.stats + i, st.v[i]);
@@ -643,10 +685,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) batch_stream_kernel(StreamA
       mbar_init(&e[i], 1);
     }
     mbar_init(reinterpret_cast<uint64_t*>(smem + lay.gbar), 1);
-    uint64_t* qb = reinterpret_cast<uint64_t*>(smem + lay.qbar);
-    for (int i = 0; i < 2 * kQueue; ++i) mbar_init(&qb[i], 1);
     uint64_t* zb = reinterpret_cast<uint64_t*>(smem + lay.zbar);
-    for (int i = 0; i < A.W; ++i) mbar_init(&zb[i], 1);
+    for (int i = 0; i <= A.W; ++i) mbar_init(&zb[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -729,8 +769,11 @@ int plan_stream(int m, int64_t n_sys, int64_t batch, int sm_count, int max_ctas,
   const int64_t T = 32 * (int64_t)m;
   const int64_t tps = (n_sys + T - 1) / T;
   if (tps > 4096) return 0;
-  int W = force_warps > 0 ? force_warps : 8;
-  int S = force_stages > 0 ? force_stages : 2;
+  // 14 compute warps with one stage each: measured 4.95 ms per 4096 x 1e5
+  // batch on B200; 8 warps x 2 stages (the first default) falls into a
+  // wait-bound mode (~19-21 ms)
+  int W = force_warps > 0 ? force_warps : 14;
+  int S = force_stages > 0 ? force_stages : 1;
   if (W > kStreamMaxWarps) W = kStreamMaxWarps;
   // shrink until one CTA fits an SM
   while (W >= 2 && stream_ctas_per_sm_m(m, W, S, (int)tps) < 1) {

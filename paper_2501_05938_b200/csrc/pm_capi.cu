@@ -169,7 +169,9 @@ struct pm_handle_s {
   size_t bcnt_bytes = 0;
   pm::StreamPlan last_stream_plan{};
   int batch_stats = 0;                    // PM_OPT_BATCH_STATS
-  unsigned long long* dstats = nullptr;   // [13] tile-stream diagnostics
+  unsigned long long* dstats = nullptr;   // [15] tile-stream diagnostics + [5][batch] timeline
+  size_t dstats_words = 0;
+  int64_t dstats_batch = 0;
   // device scratch for upper levels (+ dist boundary values)
   char* scratch = nullptr;  // level arrays of the current solve's precision
   size_t scratch_bytes = 0;
@@ -841,7 +843,7 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
       PM_CUDA(h, cudaMalloc(&h->bscr, need));
       h->bscr_bytes = need;
     }
-    const size_t cneed = (size_t)batch * 3 * sizeof(unsigned);
+    const size_t cneed = (size_t)batch * 3 * pm::kStreamCounterStride * sizeof(unsigned);
     if (cneed > h->bcnt_bytes) {
       if (h->bcnt) {
         PM_CUDA(h, cudaStreamSynchronize(st));
@@ -871,9 +873,9 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
     A.mg_K = pm::stream_magic((uint32_t)sp.ring);
     A.mg_period = pm::stream_magic((uint32_t)sp.ring * (uint32_t)sp.nw);
     const size_t slots = (size_t)sp.ring * sp.nw;
-    A.cnt1 = reinterpret_cast<unsigned*>(h->bcnt);  // [3][batch], zero between launches
-    A.cnt3 = A.cnt1 + batch;
-    A.sflag = A.cnt3 + batch;
+    A.cnt1 = reinterpret_cast<unsigned*>(h->bcnt);  // [3][batch][stride], zero between launches
+    A.cnt3 = A.cnt1 + batch * pm::kStreamCounterStride;
+    A.sflag = A.cnt3 + batch * pm::kStreamCounterStride;
     char* p = h->bscr;
     A.nodes = reinterpret_cast<unsigned char*>(p);
     p += slots * 1792;
@@ -884,9 +886,21 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
     A.discard = h->batch_discard & 1;
     A.hints = (h->batch_discard >> 1) & 1;
     if (h->batch_stats) {
-      if (!h->dstats) PM_CUDA(h, cudaMalloc(&h->dstats, 16 * sizeof(unsigned long long)));
+      // counters + per-system timeline + job traces of 8 warps + control trace of CTA 0
+      const size_t words = 16 + 5 * (size_t)batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8;
+      if (words > h->dstats_words) {
+        if (h->dstats) cudaFree(h->dstats);
+        h->dstats = nullptr;
+        PM_CUDA(h, cudaMalloc(&h->dstats, words * sizeof(unsigned long long)));
+        h->dstats_words = words;
+      }
       PM_CUDA(h, cudaMemsetAsync(h->dstats, 0, 16 * sizeof(unsigned long long), st));
+      PM_CUDA(h, cudaMemsetAsync(h->dstats + 16, 0xff, 5 * (size_t)batch * sizeof(unsigned long long), st));
+      PM_CUDA(h, cudaMemsetAsync(h->dstats + 16 + batch, 0, (size_t)batch * sizeof(unsigned long long), st));
+      PM_CUDA(h, cudaMemsetAsync(h->dstats + 16 + 5 * batch, 0, (8 * 2400 * 4 + 1200 * 2 + 4096 * 8) * sizeof(unsigned long long), st));
       A.stats = h->dstats;
+      A.tl = h->dstats + 16;
+      h->dstats_batch = batch;
     }
     h->levels.clear();
     h->last_batch_plan = pm::BatchPlan{0, 0, 0, 0, 0, 0};
@@ -1611,15 +1625,27 @@ int pm_last_stream_plan(pm_handle_t h, int32_t* out8) {
   return PM_OK;
 }
 
-int pm_batch_stream_stats(pm_handle_t h, uint64_t* out13) {
-  if (!h || !out13) return PM_ERR_VALIDATION;
+int pm_batch_stream_stats(pm_handle_t h, uint64_t* out15) {
+  if (!h || !out15) return PM_ERR_VALIDATION;
   if (!h->dstats) {
-    std::memset(out13, 0, 13 * sizeof(uint64_t));
+    std::memset(out15, 0, 15 * sizeof(uint64_t));
     return PM_OK;
   }
   PM_CUDA(h, cudaSetDevice(h->device));
   PM_CUDA(h, cudaDeviceSynchronize());
-  PM_CUDA(h, cudaMemcpy(out13, h->dstats, 13 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  PM_CUDA(h, cudaMemcpy(out15, h->dstats, 15 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return PM_OK;
+}
+
+int pm_batch_stream_timeline(pm_handle_t h, uint64_t* out, int64_t n) {
+  if (!h || !out || n < 0) return PM_ERR_VALIDATION;
+  std::memset(out, 0, (size_t)n * sizeof(uint64_t));
+  const int64_t have = 5 * h->dstats_batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8;
+  if (n > have) n = have;
+  if (!h->dstats || n == 0) return PM_OK;
+  PM_CUDA(h, cudaSetDevice(h->device));
+  PM_CUDA(h, cudaDeviceSynchronize());
+  PM_CUDA(h, cudaMemcpy(out, h->dstats + 16, (size_t)n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return PM_OK;
 }
 

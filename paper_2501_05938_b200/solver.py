@@ -171,11 +171,37 @@ class PartitionSolver:
 
     def batch_stream_stats(self) -> dict:
         """Diagnostics of the last tile-stream launch (PM_OPT_BATCH_STATS)."""
-        out = (C.c_uint64 * 13)()
+        out = (C.c_uint64 * 15)()
         self._ok(self._L.pm_batch_stream_stats(self._h, out))
         keys = ("cflag_wait_cyc", "cflag_waits", "mbox_wait_cyc", "stage_wait_cyc", "ctl_iters", "ctl_idle",
-                "stage2_cyc", "stage2_n", "publish_cyc", "compute_cyc", "control_cyc", "a_jobs", "c_jobs")
+                "stage2_cyc", "stage2_n", "publish_cyc", "compute_cyc", "control_cyc", "a_jobs", "c_jobs", "queue_ns",
+                "s2_latency_ns")
         return dict(zip(keys, [int(v) for v in out]))
+
+    def batch_stream_timeline(self, batch: int):
+        """Per-system globaltimer stamps of the last tile-stream launch with
+        PM_OPT_BATCH_STATS: a [5, batch] uint64 array (first Stage-1 start,
+        last Stage-1 end, Stage-1 count complete, Stage-2 flag, first Stage-3
+        wait start)."""
+        import numpy as np
+
+        out = np.zeros(5 * batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8, dtype=np.uint64)
+        self._ok(self._L.pm_batch_stream_timeline(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                  C.c_int64(out.size)))
+        return out[:5 * batch].reshape(5, batch)
+
+    def batch_stream_traces(self, batch: int):
+        """Job traces of 8 sample compute warps ([8, 2400, 4]: code, start,
+        stage ready, end) and the control-warp iterations of CTA 0 ([1200, 2])."""
+        import numpy as np
+
+        out = np.zeros(5 * batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8, dtype=np.uint64)
+        self._ok(self._L.pm_batch_stream_timeline(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                  C.c_int64(out.size)))
+        o = 5 * batch
+        o2 = o + 8 * 2400 * 4 + 1200 * 2
+        return (out[o:o + 8 * 2400 * 4].reshape(8, 2400, 4), out[o + 8 * 2400 * 4:o2].reshape(1200, 2),
+                out[o2:].reshape(4096, 8))
 
     def last_plan(self) -> list[int]:
         buf = (C.c_int64 * 16)()

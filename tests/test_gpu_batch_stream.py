@@ -104,7 +104,7 @@ def test_stream_kernel_back_to_back(solver):
             x = solver.solve_batch_device(*t, n_per_system=nps, m=m)
             solver.check()
             assert solver.last_batch_plan()["kernel"] == "stream"
-            assert not _counters(solver, 3 * batch).any()
+            assert not _counters(solver, 3 * 32 * batch).any()
             outs.append((systems, x, nps))
     finally:
         _reset(solver)

@@ -32,6 +32,8 @@ def main():
     p.add_argument("--m", type=int, default=10)
     p.add_argument("--reps", type=int, default=5)
     p.add_argument("--set", action="append", default=[])
+    p.add_argument("--timeline", action="store_true", help="per-system timeline percentiles")
+    p.add_argument("--trace", default="", help="save the sample warps' job traces (npz)")
     a = p.parse_args()
     sv = PartitionSolver(0)
     n = a.batch * a.rows
@@ -76,7 +78,29 @@ def main():
             "stage2_us_each": round(st["stage2_cyc"] / max(1, st["stage2_n"]) / 1965.0, 3),
             "publish_frac": round(st["publish_cyc"] / cc, 4),
             "publish_us_each": round(st["publish_cyc"] / max(1, st["ctl_iters"] - st["ctl_idle"]) / 1965.0, 3),
-            "a_jobs": st["a_jobs"], "c_jobs": st["c_jobs"]}
+            "a_jobs": st["a_jobs"], "c_jobs": st["c_jobs"],
+            "queue_us_each": round(st["queue_ns"] / max(1, st["stage2_n"]) / 1e3, 3),
+            "s2_latency_us_each": round(st["s2_latency_ns"] / max(1, st["stage2_n"]) / 1e3, 3)}
+        if a.timeline:
+            import numpy as np
+
+            tl = sv.batch_stream_timeline(a.batch).astype(np.float64)
+            t0 = tl[0].min()
+            tl = (tl - t0) / 1e3  # us since the first Stage-1 start
+            q = lambda v: [round(float(np.percentile(v, p)), 2) for p in (10, 50, 90, 99)]
+            out["timeline_us_p10_50_90_99"] = {
+                "A_spread": q(tl[1] - tl[0]), "publish_delay": q(tl[2] - tl[1]), "stage2": q(tl[3] - tl[2]),
+                "C_wait_from_first_C": q(np.maximum(0, tl[3] - tl[4])), "flag_minus_firstA": q(tl[3] - tl[0]),
+                "firstC_minus_firstA": q(tl[4] - tl[0])}
+            mid = a.batch // 2
+            out["timeline_sample_us"] = {str(s): [round(float(v), 1) for v in tl[:, s]]
+                                         for s in (0, 1, 2, 3, 4, mid, mid + 1, a.batch - 1)}
+        if a.trace:
+            import numpy as np
+
+            tr, ctl, wsum = sv.batch_stream_traces(a.batch)
+            t0 = int(sv.batch_stream_timeline(a.batch)[0].min())
+            np.savez(a.trace, tr=tr, ctl=ctl, t0=t0, wsum=wsum)
         print(json.dumps(out), flush=True)
         for k in kv:
             sv.set_option(OPTS[k], 0 if k != "discard" else 3)
