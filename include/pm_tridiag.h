@@ -123,7 +123,10 @@ typedef struct pm_model_bundle {
                                   (both of 128 x 8 CTA tiles, level 2 one tile)
                                   in one launch, one co-resident CTA per level-1
                                   tile: reduce, last CTA solves level 2, each
-                                  back-solves its tile (3 launches -> 1); 0: off */
+                                  back-solves its tile (3 launches -> 1); 0: off;
+                                  2: also a row-sharded rank's upper levels in
+                                  two launches (level 1 of 8-row blocks + the
+                                  chain of its tile segments; pm_dist_*)        */
 #define PM_OPT_BATCH_LAG 25    /* tile-stream kernel: rounds Stage 3 trails Stage 1
                                   (0 = plan, >= stages + 1)                        */
 #define PM_OPT_BATCH_DISCARD 26 /* tile-stream kernel: bit 0 discards consumed

@@ -98,6 +98,12 @@ struct Prec<double> {
   static cudaError_t dist_chain(const double* ia, int w, int r, double* xb, int* f, cudaStream_t st) {
     return pm::launch_dist_chain(ia, w, r, xb, f, st);
   }
+  using DistUpperArgs = pm::DistUpperArgs;
+  static int dist_upper_capacity(int sm) { return pm::dist_upper_capacity(sm); }
+  static size_t dist_tree2_bytes() { return pm::dist_tree2_bytes(); }
+  static cudaError_t dist_upper(int mode, const DistUpperArgs& u, int sm, cudaStream_t st, int* g) {
+    return pm::launch_dist_upper(mode, u, sm, st, g);
+  }
   static cudaError_t generate(double* a, double* b, double* c, double* d, int64_t n, int64_t r0,
                               int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
     return pm::launch_generate(a, b, c, d, n, r0, cnt, seed, sm, st);
@@ -129,6 +135,12 @@ struct Prec<float> {
   }
   static cudaError_t dist_chain(const float* ia, int w, int r, float* xb, int* f, cudaStream_t st) {
     return pm32::launch_dist_chain(ia, w, r, xb, f, st);
+  }
+  using DistUpperArgs = pm32::DistUpperArgs;
+  static int dist_upper_capacity(int sm) { return pm32::dist_upper_capacity(sm); }
+  static size_t dist_tree2_bytes() { return pm32::dist_tree2_bytes(); }
+  static cudaError_t dist_upper(int mode, const DistUpperArgs& u, int sm, cudaStream_t st, int* g) {
+    return pm32::launch_dist_upper(mode, u, sm, st, g);
   }
   static cudaError_t generate(float* a, float* b, float* c, float* d, int64_t n, int64_t r0,
                               int64_t cnt, uint64_t seed, int sm, cudaStream_t st) {
@@ -179,6 +191,12 @@ struct pm_handle_s {
   unsigned long long* dsync = nullptr;  // counters of the fused upper-level kernel
   int upper_fused = 1;                  // PM_OPT_UPPER_FUSED
   int upper_cap[2] = {-1, -1};          // its co-resident CTAs (FP64, FP32; -1: not queried)
+  // row-sharded ranks: level 1 + the chain of its tile segments in two
+  // launches (pm::launch_dist_upper); set by build_plan
+  bool dist_fused = false;
+  int dist_chain = 1;                   // level-2 segments per thread
+  void* dist_seg2 = nullptr;            // [G][8] | [G][8] nodes | [G][2] x, in the level scratch
+  int dist_cap[2] = {-1, -1};
   // device staging for the host path: a, b, c, d, x
   char* hbuf = nullptr;
   size_t hbuf_bytes = 0;
@@ -310,7 +328,7 @@ void set_warp_tiles(pm_handle_t h, Level& L) {
 template <class R>
 int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R* c,
                const R* d, R* x, bool ragged0, size_t extra_elems,
-               bool allow_chain = true, int nparts = 1) {
+               bool allow_chain = true, int nparts = 1, int dist_world = 0) {
   std::vector<Level> lv;
   Level L0;
   L0.n = n;
@@ -343,6 +361,9 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
   }
   L0.T = (int64_t)L0.P * m;
   L0.ntiles = (n + L0.T - 1) / L0.T;
+  // a ragged rank whose rows fill whole tiles never pads: it runs the padded
+  // (single-system) kernel variants, whose tree bounds are constants
+  if (ragged0 && n % L0.T == 0) L0.pad_mode = 1;
   lv.push_back(L0);
   // Chain mode (single system / batch on warp tiles): level 0's tiles form C
   // contiguous chunks (C = the Stage-3 kernel's resident warps); each warp
@@ -382,11 +403,38 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
     if (U.m > PM_MAX_M) return fail(h, PM_ERR_RUNTIME, "chain root too large");
     lv.push_back(U);
   }
+  // Row-sharded rank (dist_world > 0): level 1 of 128 x 8 CTA tiles, one
+  // co-resident CTA each, and the chain of their G segments (two launches,
+  // pm::launch_dist_upper) when level 1 holds whole 8-row blocks (a non-last
+  // rank cannot pad), G fits the chain and the device, and G > 1.
+  h->dist_fused = false;
+  if (dist_world > 0 && dist_world <= pm::kDistMaxWorld && h->upper_fused >= 2 && !h->robust_mode && !h->chain &&
+      L0.warps_per_cta > 0 && L0.ntiles > 1) {
+    const int64_t n1 = 2 * L0.ntiles;
+    const int64_t T1 = (int64_t)pm::kUpperP * pm::kUpperM;
+    const int64_t G = (n1 + T1 - 1) / T1;
+    int& cap = h->dist_cap[sizeof(R) == 4];
+    if (cap < 0) cap = Prec<R>::dist_upper_capacity(h->sm_count);
+    if (G > 1 && G <= (int64_t)pm::kUpperP * pm::kDistChainMax && G <= cap && !(ragged0 && n1 % pm::kUpperM)) {
+      Level U;
+      U.n = n1;
+      U.m = pm::kUpperM;
+      U.P = pm::kUpperP;
+      U.T = T1;
+      U.ntiles = G;
+      U.pad_mode = ragged0 ? 0 : 1;
+      U.bulk = true;
+      U.stages = 1;
+      lv.push_back(U);
+      h->dist_fused = true;
+      h->dist_chain = (int)((G + pm::kUpperP - 1) / pm::kUpperP);
+    }
+  }
   // Upper levels: warp tiles of 32*upper_m rows while the level exceeds one
   // ROOT tile (128*root_m rows), then the ROOT; ragged ranks use CTA tiles
   // with m = 2.
   const int m_up = ragged0 ? 2 : h->upper_cta_m;
-  while (lv.back().ntiles > 1) {
+  while (!h->dist_fused && lv.back().ntiles > 1) {
     const Level& prev = lv.back();
     Level U;
     U.n = 2 * prev.ntiles;
@@ -419,10 +467,17 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
     nodes_off = (total + 31) / 32 * 32;
     total = nodes_off + (size_t)L0.ntiles * 8;  // 7 reals per Node, padded to 8
   }
+  size_t seg2_off = 0;
+  if (h->dist_fused) {
+    seg2_off = (total + 31) / 32 * 32;
+    // segments, chain nodes, boundary pairs | level 2's CTA tree
+    total = seg2_off + (size_t)lv[1].ntiles * 18 + (Prec<R>::dist_tree2_bytes() + 2 * sizeof(R)) / sizeof(R);
+  }
   int st = ensure_scratch(h, total * sizeof(R));
   if (st) return st;
   R* scr = reinterpret_cast<R*>(h->scratch);
   h->chain_nodes = h->chain ? (void*)(scr + nodes_off) : nullptr;
+  h->dist_seg2 = h->dist_fused ? (void*)(scr + seg2_off) : nullptr;
   for (size_t k = 1; k < lv.size(); ++k) {
     const size_t stride = (size_t)((lv[k].n + 31) / 32 * 32);
     R* base = scr + off[k];
@@ -606,6 +661,54 @@ int enq_upper_fused(pm_handle_t h, size_t k, cudaStream_t st) {
   if (timed) {
     cudaEventRecord(h->kev[ev + 1], st);
     h->krec.push_back({3, (int)k, ev});
+  }
+  if (grid > 0) ++h->launches;
+  return PM_OK;
+}
+
+// Row-sharded rank, fused plan: level 1 + the level-2 chain in one launch
+// (mode kModeReduce: -> iface or the P2P publish; kModeSolve: iface_all or
+// the P2P acquire -> level 1's x).
+template <class R>
+int enq_dist_upper(pm_handle_t h, int mode, bool zf, bool zl, int rank, int world, R* iface,
+                   const R* iface_all, bool p2p, cudaStream_t st) {
+  const Level& L1 = h->levels[1];
+  typename Prec<R>::DistUpperArgs u;
+  u.a1 = static_cast<const R*>(L1.a); u.b1 = static_cast<const R*>(L1.b);
+  u.c1 = static_cast<const R*>(L1.c); u.d1 = static_cast<const R*>(L1.d);
+  u.x1 = static_cast<R*>(L1.x);
+  u.n1 = L1.n;
+  const size_t G = (size_t)L1.ntiles;
+  R* base = static_cast<R*>(h->dist_seg2);
+  u.seg2 = base;
+  u.node2 = base + 8 * G;
+  u.x2 = base + 16 * G;
+  u.tree2 = base + 18 * G;
+  u.chain = h->dist_chain;
+  u.ragged = L1.pad_mode == 0;
+  u.zero_first = zf;
+  u.zero_last = zl;
+  u.iface = iface;
+  u.iface_all = iface_all;
+  u.rank = rank;
+  u.world = world;
+  if (p2p) {
+    u.xpeers = h->d_peers;
+    u.xlocal = h->xbuf;
+    u.xepoch = h->p2p_top.epoch;
+    u.xtimeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s
+  }
+  u.sync = h->dsync;
+  u.flag = h->dflag;
+  const bool timed = h->ktimes && next_kevent(h) != nullptr;
+  const size_t ev = h->krec.size() * 2;
+  if (timed) cudaEventRecord(h->kev[ev], st);
+  int grid = 0;
+  const cudaError_t e = Prec<R>::dist_upper(mode, u, h->sm_count, st, &grid);
+  if (e != cudaSuccess) return cuda_fail(h, e, "row-sharded upper-level kernel launch");
+  if (timed) {
+    cudaEventRecord(h->kev[ev + 1], st);
+    h->krec.push_back({mode == pm::kModeReduce ? 5 : 6, 1, ev});
   }
   if (grid > 0) ++h->launches;
   return PM_OK;
@@ -1162,10 +1265,14 @@ int dist_reduce_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   PM_CUDA(h, cudaSetDevice(h->device));
   h->launches = 0;
   // same plan (and the same 32-R prefix) as pm_dist_solve_f64
-  if ((r = build_plan<R>(h, n_local, m, a, b, c, d, const_cast<R*>(d), !last, 32, false))) return r;
+  if ((r = build_plan<R>(h, n_local, m, a, b, c, d, const_cast<R*>(d), !last, 32, false, 1, world))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
   const bool zf = rank == 0, zl = last;
+  if (h->dist_fused) {
+    if ((r = enq_reduce<R>(h, 0, 0, h->levels[0].ntiles, st, zf, zl, 0, nullptr))) return r;
+    return enq_dist_upper<R>(h, pm::kModeReduce, zf, zl, rank, world, iface, nullptr, h->p2p_top.active, st);
+  }
   const size_t top = h->levels.size() - 1;
   for (size_t k = 0; k < top; ++k)
     if ((r = enq_reduce<R>(h, k, 0, h->levels[k].ntiles, st, zf, zl, 0, nullptr))) return r;
@@ -1190,11 +1297,21 @@ int dist_solve_impl(pm_handle_t h, const R* a, const R* b, const R* c,
   PM_CUDA(h, cudaSetDevice(h->device));
   h->launches = 0;
   // two extra doubles in front of the level scratch hold this rank's (xf, xl)
-  if ((r = build_plan<R>(h, n_local, m, a, b, c, d, x, !last, 32, false))) return r;
+  if ((r = build_plan<R>(h, n_local, m, a, b, c, d, x, !last, 32, false, 1, world))) return r;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->last_stream = st;
   R* xb = reinterpret_cast<R*>(h->scratch);  // extra_elems region
   const bool zf = rank == 0, zl = last;
+  if (h->dist_fused) {
+    if (flags) {
+      h->p2p_top.active = true;
+      h->p2p_top.epoch = epoch;
+    }
+    r = enq_dist_upper<R>(h, pm::kModeSolve, zf, zl, rank, world, nullptr, iface_all, flags != nullptr, st);
+    h->p2p_top.active = false;
+    if (r) return r;
+    return enq_solve<R>(h, 0, 0, h->levels[0].ntiles, st, zf, zl, 0, nullptr);
+  }
   const size_t top = h->levels.size() - 1;
   if (flags) {  // P2P: the top-level SOLVE acquires and chains the interface rows itself
     h->p2p_top.active = true;
@@ -1570,7 +1687,8 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       h->upper_cta_p = (int)value;
       return PM_OK;
     case PM_OPT_UPPER_FUSED:
-      h->upper_fused = value ? 1 : 0;
+      if (value < 0 || value > 2) return fail(h, PM_ERR_VALIDATION, "upper fused must be 0, 1 or 2");
+      h->upper_fused = (int)value;
       return PM_OK;
     case PM_OPT_PAIR_STAGES:
       if (value < 1 || value > 4) return fail(h, PM_ERR_VALIDATION, "pair stages must lie in [1, 4]");

@@ -196,6 +196,36 @@ __device__ void p2p_publish(const Seg& top, const TileArgs& A) {
   }
 }
 
+// One thread: chain the W ranks' interface segments (per rank [Fa, La, Fb, Lb,
+// Fc, Lc, Fd, Ld]) keeping the nodes, solve the final 2x2 (rank 0's F.a and
+// rank W-1's L.c are zero), walk back to `rank`: its (x_first, x_last).
+__device__ void chain_iface(const real* iface, int W, int rank, real& xf, real& xl, bool& bad) {
+  auto seg_of = [&](int k) {
+    const real* p = iface + 8 * k;
+    return Seg{Row{p[0], p[2], p[4], p[6]}, Row{p[1], p[3], p[5], p[7]}};
+  };
+  Node cn[kMaxP2PWorld];
+  Seg acc = seg_of(0);
+  for (int k = 1; k < W; ++k) combine(acc, seg_of(k), acc, cn[k], bad);
+  const real det = fma(acc.F.b, acc.L.b, -acc.F.c * acc.L.a);
+  bad |= (det == 0.0);
+  const real inv = drcp(det);
+  const real x0 = fma(acc.F.d, acc.L.b, -acc.F.c * acc.L.d) * inv;
+  real xr = fma(acc.F.b, acc.L.d, -acc.L.a * acc.F.d) * inv;
+  real xfr = x0;
+  for (int k = W - 1; k >= 1 && k >= rank; --k) {
+    real xl_prev, xf_k;
+    split_node(cn[k], x0, xr, xl_prev, xf_k);
+    if (k == rank) {
+      xfr = xf_k;
+      break;
+    }
+    xr = xl_prev;
+  }
+  xf = xfr;
+  xl = xr;
+}
+
 // Thread 0 of a rank's top-level SOLVE: wait for every rank's rows, chain the
 // 2*world-row interface system, solve its 2x2, walk back to this rank.
 // Returns false on a timeout (flag bit 4).
@@ -213,30 +243,7 @@ __device__ bool p2p_chain(const TileArgs& A, real& xf, real& xl, bool& bad) {
       __nanosleep(256);
     }
   }
-  auto seg_of = [&](int k) {
-    const real* p = iface + 8 * k;
-    return Seg{Row{p[0], p[2], p[4], p[6]}, Row{p[1], p[3], p[5], p[7]}};
-  };
-  Node cn[kMaxP2PWorld];
-  Seg acc = seg_of(0);
-  for (int k = 1; k < W; ++k) combine(acc, seg_of(k), acc, cn[k], bad);
-  const real det = fma(acc.F.b, acc.L.b, -acc.F.c * acc.L.a);
-  bad |= (det == 0.0);
-  const real inv = drcp(det);
-  const real x0 = fma(acc.F.d, acc.L.b, -acc.F.c * acc.L.d) * inv;
-  real xr = fma(acc.F.b, acc.L.d, -acc.L.a * acc.F.d) * inv;
-  real xfr = x0;
-  for (int k = W - 1; k >= 1 && k >= A.xrank; --k) {
-    real xl_prev, xf_k;
-    split_node(cn[k], x0, xr, xl_prev, xf_k);
-    if (k == A.xrank) {
-      xfr = xf_k;
-      break;
-    }
-    xr = xl_prev;
-  }
-  xf = xfr;
-  xl = xr;
+  chain_iface(iface, W, A.xrank, xf, xl, bad);
   return true;
 }
 
@@ -634,6 +641,276 @@ cudaError_t launch_upper_fused(const UpperArgs& u, int sm_count, cudaStream_t st
   cfg.numAttrs = na;
   if (grid_out) *grid_out = (int)tiles;
   return cudaLaunchKernelEx(&cfg, upper_fused_kernel, u);
+}
+
+// ---------------------------------------------------------------------------
+// Row-sharded ranks: upper levels in two launches (see DistUpperArgs).  A
+// rank's plan was REDUCE(0), REDUCE(1..3) with 2-row blocks (a non-last rank
+// cannot pad its last tile: the coupling to the next rank must survive),
+// exchange, SOLVE(3..1), SOLVE(0): 8 launches + the chain kernel, 2.5-4 %
+// above the single-system solve.  Here level 1 keeps 8-row blocks (whole
+// blocks only: n1 % 8 == 0 on a non-last rank) and level 2 is a segment
+// chain, which has no block size and therefore no padding question at all.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ TileArgs dist_p2p_args(const DistUpperArgs& u) {
+  TileArgs t;
+  t.flag = u.flag;
+  t.xpeers = u.xpeers;
+  t.xlocal = u.xlocal;
+  t.xworld = u.world;
+  t.xrank = u.rank;
+  t.xepoch = u.xepoch;
+  t.xtimeout_ns = u.xtimeout_ns;
+  return t;
+}
+
+// This CTA's level-1 tile: rows into shared memory (kept), Stage 1 of every
+// 8-row block, CTA tree (nodes kept when `keep`).  Returns the tile's segment
+// in thread 0 and the tile's non-empty block count in nblk.
+__device__ __forceinline__ Seg dist_tile_reduce(const DistUpperArgs& u, UpperSmem& sm, int64_t t, bool keep,
+                                                TileCtx& ctx, int& nblk, bool& bad) {
+  constexpr int T = kUpperP * kUpperM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ctx = upper_ctx(u.a1, u.b1, u.c1, u.d1, u.n1, t);
+  ctx.zf = u.zero_first != 0;
+  ctx.zl = u.zero_last != 0;
+  for (int i = tid; i < T; i += kUpperP) {
+    const bool in = i < ctx.valid;
+    const int64_t g = ctx.row0 + i;
+    sm.rows[0][i] = in ? __ldcg(u.a1 + g) : real(0);
+    sm.rows[1][i] = in ? __ldcg(u.b1 + g) : real(0);
+    sm.rows[2][i] = in ? __ldcg(u.c1 + g) : real(0);
+    sm.rows[3][i] = in ? __ldcg(u.d1 + g) : real(0);
+  }
+  __syncthreads();
+  RegAcc<kUpperM> regs;
+  regs.load(sm.rows[0], sm.rows[1], sm.rows[2], sm.rows[3], tid * kUpperM, ctx);
+  const Seg seg = block_reduce_fast<kUpperM, false>(regs, bad);
+  nblk = u.ragged ? (ctx.valid + kUpperM - 1) / kUpperM : kUpperP;
+  return cta_upsweep(seg, sm.tree[0], keep ? sm.wnodes[0] : nullptr, lane, warp, kUpperP / 32, nblk, bad);
+}
+
+__device__ __forceinline__ Seg ld_seg(const real* p) {
+  return Seg{Row{__ldcg(p), __ldcg(p + 1), __ldcg(p + 2), __ldcg(p + 3)},
+             Row{__ldcg(p + 4), __ldcg(p + 5), __ldcg(p + 6), __ldcg(p + 7)}};
+}
+__device__ __forceinline__ void st_seg(real* p, const Seg& s) {
+  p[0] = s.F.a; p[1] = s.F.b; p[2] = s.F.c; p[3] = s.F.d;
+  p[4] = s.L.a; p[5] = s.L.b; p[6] = s.L.c; p[7] = s.L.d;
+}
+
+// Level 2: thread i chains segments [i*C, min(G, (i+1)*C)) (nodes to node2
+// when keep), then the CTA tree (nodes kept in tree[1] / wnodes[1] when keep).
+__device__ __forceinline__ Seg dist_level2_up(const DistUpperArgs& u, UpperSmem& sm, int G, bool keep,
+                                              int& nblk2, bool& bad) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int C = u.chain;
+  const int lo = tid * C, hi = min(G, lo + C);
+  Seg acc{};
+  if (lo < hi) {
+    acc = ld_seg(u.seg2 + (size_t)8 * lo);
+    Seg nx = (lo + 1 < hi) ? ld_seg(u.seg2 + (size_t)8 * (lo + 1)) : acc;
+    for (int i = lo + 1; i < hi; ++i) {
+      const Seg cur = nx;
+      if (i + 1 < hi) nx = ld_seg(u.seg2 + (size_t)8 * (i + 1));  // next load in flight over the combine
+      Node nd;
+      combine(acc, cur, acc, nd, bad);
+      if (keep) {
+        real* q = u.node2 + (size_t)8 * i;
+        q[0] = nd.p0; q[1] = nd.p1; q[2] = nd.p2; q[3] = nd.q0; q[4] = nd.q1; q[5] = nd.q2; q[6] = nd.r;
+      }
+    }
+  }
+  nblk2 = (G + C - 1) / C;
+  return cta_upsweep(acc, sm.tree[1], keep ? sm.wnodes[1] : nullptr, lane, warp, kUpperP / 32, nblk2, bad);
+}
+
+// Level 2's CTA tree (tree[1] + wnodes[1]) between the two launches: the
+// REDUCE's last CTA builds it, the SOLVE's CTA 0 splits it.
+size_t dist_tree2_bytes() { return sizeof(TreeSmem) + sizeof(Node) * (kUpperP / 32) * 31; }
+__device__ __forceinline__ void tree2_copy(UpperSmem& sm, real* g, bool to_global) {
+  constexpr int W1 = sizeof(TreeSmem) / 4, W2 = sizeof(Node) * (kUpperP / 32) * 31 / 4;
+  static_assert(sizeof(TreeSmem) % 4 == 0 && (sizeof(Node) * (kUpperP / 32) * 31) % 4 == 0, "word copy");
+  unsigned* t = reinterpret_cast<unsigned*>(&sm.tree[1]);
+  unsigned* w = reinterpret_cast<unsigned*>(&sm.wnodes[1][0]);
+  unsigned* gg = reinterpret_cast<unsigned*>(g);
+  for (int i = threadIdx.x; i < W1 + W2; i += kUpperP) {
+    unsigned* sp = (i < W1) ? t + i : w + (i - W1);
+    if (to_global) gg[i] = *sp;
+    else *sp = __ldcg(gg + i);
+  }
+}
+
+__global__ void __launch_bounds__(kUpperP, 4) dist_upper_reduce_kernel(DistUpperArgs u) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  UpperSmem& sm = *reinterpret_cast<UpperSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int64_t t = blockIdx.x;
+  const int G = gridDim.x;
+  bool bad = false;
+  pdl_wait();
+  pdl_launch_dependents();
+  TileCtx ctx;
+  int nblk = 0;
+  const Seg top = dist_tile_reduce(u, sm, t, false, ctx, nblk, bad);
+  if (tid == 0) {
+    st_seg(u.seg2 + (size_t)8 * t, top);
+    __threadfence();
+    const unsigned long long ticket = atomicAdd(u.sync, 1ull);
+    sm.last = (ticket == (unsigned long long)G - 1);
+    if (sm.last) {
+      atomicExch(u.sync, 0ull);
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (sm.last) {
+    int nblk2 = 0;
+    const Seg top2 = dist_level2_up(u, sm, G, true, nblk2, bad);
+    __syncthreads();
+    tree2_copy(sm, u.tree2, true);  // ordered before the SOLVE launch (kernel boundary)
+    if (tid == 0) {
+      if (u.xpeers) {
+        p2p_publish(top2, dist_p2p_args(u));
+      } else {
+        const real v[8] = {top2.F.a, top2.L.a, top2.F.b, top2.L.b, top2.F.c, top2.L.c, top2.F.d, top2.L.d};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u.iface[j] = v[j];
+      }
+    }
+  }
+  if (bad) atomicOr(u.flag, 1);
+}
+
+__global__ void __launch_bounds__(kUpperP, 4) dist_upper_solve_kernel(DistUpperArgs u) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  UpperSmem& sm = *reinterpret_cast<UpperSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t t = blockIdx.x;
+  const int G = gridDim.x;
+  bool bad = false;
+  pdl_wait();
+  pdl_launch_dependents();
+  if (blockIdx.x == 0) {
+    // level 2's tree from the REDUCE, the rank's boundary values, then every
+    // tile's pair
+    const int nblk2 = (G + u.chain - 1) / u.chain;
+    tree2_copy(sm, u.tree2, false);
+    __syncthreads();
+    real xf = 0.0, xl = 0.0;
+    if (tid == 0) {
+      if (u.xpeers) p2p_chain(dist_p2p_args(u), xf, xl, bad);
+      else chain_iface(u.iface_all, u.world, u.rank, xf, xl, bad);
+    }
+    __syncthreads();
+    cta_downsweep(xf, xl, sm.tree[1], sm.wnodes[1], lane, warp, kUpperP / 32, nblk2);
+    const int C = u.chain;
+    const int lo = tid * C, hi = min(G, lo + C);
+    if (lo < hi) {
+      real xrun = xl;
+      auto ld_node = [&](int i) {
+        const real* q = u.node2 + (size_t)8 * i;
+        return Node{__ldcg(q), __ldcg(q + 1), __ldcg(q + 2), __ldcg(q + 3), __ldcg(q + 4), __ldcg(q + 5),
+                    __ldcg(q + 6)};
+      };
+      Node nx = (hi - 1 > lo) ? ld_node(hi - 1) : Node{};
+      for (int i = hi - 1; i > lo; --i) {
+        const Node nd = nx;
+        if (i - 1 > lo) nx = ld_node(i - 1);  // next node in flight over the split
+        real xl_prev, xf_i;
+        split_node(nd, xf, xrun, xl_prev, xf_i);
+        u.x2[2 * i] = xf_i;
+        u.x2[2 * i + 1] = xrun;
+        xrun = xl_prev;
+      }
+      u.x2[2 * lo] = xf;
+      u.x2[2 * lo + 1] = xrun;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(u.sync + 1, 1ull);  // level 2's pairs are out
+  }
+  TileCtx ctx;
+  int nblk = 0;
+  (void)dist_tile_reduce(u, sm, t, true, ctx, nblk, bad);
+  real xf = 0.0, xl = 0.0;
+  if (tid == 0) {
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_gpu_u64(u.sync + 1) == 0) {
+      if (global_ns() - t0 > kFusedWaitTimeoutNs) {
+        atomicOr(u.flag, 8);
+        break;
+      }
+      __nanosleep(32);
+    }
+    xf = __ldcg(u.x2 + 2 * t);
+    xl = __ldcg(u.x2 + 2 * t + 1);
+    if (atomicAdd(u.sync + 2, 1ull) == (unsigned long long)G - 1) {  // the last CTA re-arms the flag
+      atomicExch(u.sync + 1, 0ull);
+      atomicExch(u.sync + 2, 0ull);
+    }
+  }
+  RegAcc<kUpperM> regs;
+  regs.load(sm.rows[0], sm.rows[1], sm.rows[2], sm.rows[3], tid * kUpperM, ctx);
+  __syncthreads();
+  cta_downsweep(xf, xl, sm.tree[0], sm.wnodes[0], lane, warp, kUpperP / 32, nblk);
+  block_interior<kUpperM>(regs, kUpperM, xf, xl, bad);
+  const int64_t g0 = t * (kUpperP * kUpperM) + tid * kUpperM;
+#pragma unroll
+  for (int j = 0; j < kUpperM; ++j) {
+    if (g0 + j < u.n1) {
+      bad |= !isfinite(regs.x(j));
+      u.x1[g0 + j] = regs.x(j);
+    }
+  }
+  if (bad) atomicOr(u.flag, 1);
+}
+
+int dist_upper_capacity(int sm_count) {
+  const size_t smem = upper_smem_bytes();
+  int cap = 1 << 30;
+  for (auto kern : {dist_upper_reduce_kernel, dist_upper_solve_kernel}) {
+    int per_sm = 0;
+    if (ensure_smem_attr(kern, smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kUpperP, smem) != cudaSuccess)
+      return 0;
+    cap = per_sm * sm_count < cap ? per_sm * sm_count : cap;
+  }
+  return cap;
+}
+
+cudaError_t launch_dist_upper(int mode, const DistUpperArgs& u, int sm_count, cudaStream_t st, int* grid_out) {
+  constexpr int64_t T = (int64_t)kUpperP * kUpperM;
+  const int64_t tiles = (u.n1 + T - 1) / T;
+  if (tiles < 1 || tiles > (int64_t)kUpperP * u.chain || u.chain < 1 || u.chain > kDistChainMax)
+    return cudaErrorInvalidValue;
+  if (u.ragged && (u.n1 % kUpperM) != 0) return cudaErrorInvalidValue;
+  if (u.world < 1 || u.world > kDistMaxWorld) return cudaErrorInvalidValue;
+  auto kern = (mode == kModeReduce) ? dist_upper_reduce_kernel : dist_upper_solve_kernel;
+  const size_t smem = upper_smem_bytes();
+  cudaError_t e = ensure_smem_attr(kern, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kUpperP, smem) != cudaSuccess ||
+      tiles > (int64_t)per_sm * sm_count)
+    return cudaErrorInvalidConfiguration;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)tiles);
+  cfg.blockDim = dim3(kUpperP);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeCooperative;  // the SOLVE's flag wait needs every CTA resident
+  attr[na++].val.cooperative = 1;
+  if (g_use_pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (grid_out) *grid_out = (int)tiles;
+  return cudaLaunchKernelEx(&cfg, kern, u);
 }
 
 // ---------------------------------------------------------------------------

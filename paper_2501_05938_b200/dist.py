@@ -23,7 +23,11 @@ def split_rows(n: int, world: int, m: int) -> list[int]:
         raise ValidationError("need n >= 1 and world >= 1")
     if world == 1:
         return [n]
-    q = max(m, (n // world) // m * m)
+    # non-last ranks: whole level-0 tiles in groups of 4 (128*m rows) when the
+    # share allows, so level 1 holds whole 8-row blocks and the rank's upper
+    # levels run fused (two launches); else a multiple of m
+    unit = 128 * m if n // world >= 128 * m else m
+    q = max(m, (n // world) // unit * unit)
     last = n - q * (world - 1)
     if last < 1:
         raise ValidationError(f"n = {n} too small for {world} ranks with m = {m}")

@@ -485,6 +485,91 @@ def test_dist_p2p_virtual_ranks(solver, world, n, m):
         h.close()
 
 
+def _dist_run(solver, rows, m, seed, p2p, reps=1, fused=2):
+    """Virtual ranks with explicit row counts; returns (x, [(reduce, solve)
+    launches], plans) after checking x against the oracle."""
+    import torch
+
+    from paper_2501_05938_b200 import PartitionSolver
+    from paper_2501_05938_b200.solver import PM_OPT_UPPER_FUSED
+
+    world = len(rows)
+    handles = [solver] + [PartitionSolver(0) for _ in range(world - 1)]
+    for h in handles:
+        h.set_option(PM_OPT_UPPER_FUSED, fused)
+    n = sum(rows)
+    ah, bh, ch, dh = oracle.generate(n, seed)
+    offs = np.concatenate([[0], np.cumsum(rows)])
+    loc = [[torch.from_numpy(v[offs[r]:offs[r + 1]].copy()).cuda() for v in (ah, bh, ch, dh)]
+           for r in range(world)]
+    if p2p:
+        bufs = [h.dist_exchange_alloc(world) for h in handles]
+        for r, h in enumerate(handles):
+            h.dist_set_peers(bufs, r)
+    iface_all = torch.zeros(8 * world, dtype=torch.float64, device="cuda")
+    launches, plans = [], []
+    try:
+        for _ in range(reps):
+            red = []
+            for r in range(world):
+                if p2p:
+                    handles[r].dist_reduce_p2p(*loc[r], m=m)
+                else:
+                    handles[r].dist_reduce(*loc[r], m=m, rank=r, world=world, iface=iface_all[8 * r:8 * r + 8])
+                red.append(handles[r].last_launch_count)
+            xs = []
+            launches = []
+            for r in range(world):
+                x = torch.empty(rows[r], dtype=torch.float64, device="cuda")
+                if p2p:
+                    handles[r].dist_solve_p2p(*loc[r], x, m=m)
+                else:
+                    handles[r].dist_solve(*loc[r], x, m=m, rank=r, world=world, iface_all=iface_all)
+                launches.append((red[r], handles[r].last_launch_count))
+                xs.append(x)
+            plans = [h.last_plan() for h in handles]
+            for h in handles:
+                h.check()
+            _check(torch.cat(xs).cpu().numpy(), ah, bh, ch, dh)
+    finally:
+        solver.set_option(PM_OPT_UPPER_FUSED, 1)
+        for h in handles[1:]:
+            h.close()
+    return launches, plans
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+@pytest.mark.parametrize("world,per_rank,m", [(2, 1_000_000, 10), (3, 700_000, 8), (8, 400_000, 10),
+                                               (2, 2_621_440, 10), (4, 300_000, 2)])
+def test_dist_fused_upper_levels(solver, p2p, world, per_rank, m):
+    """Row-sharded ranks whose level 1 holds whole 8-row blocks (split_rows:
+    non-last ranks own a multiple of 128 m rows) run their upper levels, with
+    PM_OPT_UPPER_FUSED = 2, as two launches (level 1 + the chain of its tile segments): REDUCE(0) + upper
+    reduce, upper solve + SOLVE(0).  Parity with the oracle, three solves in a
+    row (counters re-armed, P2P parities), every rank's plan two levels."""
+    from paper_2501_05938_b200.dist import split_rows
+
+    n = world * per_rank + 12_345 * m // 10 * 2
+    rows = split_rows(n, world, m)
+    assert all(r % (128 * m) == 0 for r in rows[:-1])
+    launches, plans = _dist_run(solver, rows, m, 29, p2p, reps=3)
+    for r, (lr, ls) in enumerate(launches):
+        assert len(plans[r]) == 2, plans[r]
+        assert (lr, ls) == (2, 2), launches
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+def test_dist_fused_upper_fallback_and_mixed(solver, p2p):
+    """A non-last rank whose level 1 is not whole 8-row blocks keeps the
+    2-row-block levels; mixed plans across ranks still chain correctly."""
+    m = 10
+    rows = [32 * m * 4001, m * 64_000, m * 50_003 + 7]  # rank 0: 4001 tiles -> n1 = 8002, not 8-row blocks
+    launches, plans = _dist_run(solver, rows, m, 31, p2p, reps=2)
+    assert len(plans[0]) > 2  # fallback plan
+    assert len(plans[1]) == 2  # fused
+    assert launches[1] == (2, 2)
+
+
 def _cudart():
     import ctypes as C
     import glob

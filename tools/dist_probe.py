@@ -20,7 +20,11 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--rows", type=float, default=8e7)
     p.add_argument("--world", type=int, default=2)
-    p.add_argument("--reps", type=int, default=20)
+    p.add_argument("--reps", type=int, default=10)
+    p.add_argument("--cooldown", type=float, default=0.5, help="idle seconds before every measurement")
+    p.add_argument("--rounds", type=int, default=0, help="repeat single / rank 0 / last rank this many times")
+    p.add_argument("--ab", type=int, default=0,
+                   help="rounds of an interleaved A/B/C of PM_OPT_UPPER_FUSED 2 / 1 / 0 (median per variant)")
     args = p.parse_args()
     n, m, W = int(args.rows), 10, args.world
     s = PartitionSolver(0)
@@ -30,6 +34,13 @@ def main():
     st = torch.cuda.current_stream()
 
     def timed(fn):
+        # B200 holds its burst clocks for ~40-50 ms of back-to-back solves, then
+        # the power limit takes ~10 % (measured: 0.883 -> 0.99 ms per 8e7
+        # solve); every measurement starts from an idle GPU and stays short
+        import time
+
+        torch.cuda.synchronize()
+        time.sleep(args.cooldown)
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
@@ -59,6 +70,34 @@ def main():
         s.set_option(PM_OPT_KERNEL_TIMES, 0)
         out[f"rank{r}_launches"] = s.last_launch_count
         out[f"rank{r}_plan"] = s.last_plan()
+    if args.rounds:
+        res = {}
+        for _ in range(args.rounds):
+            res.setdefault("single", []).append(timed(lambda: s.solve_device(a, b, c, d, m=m, out=x)))
+            for r in (0, W - 1):
+                def one():
+                    s.dist_reduce(a, b, c, d, m=m, rank=r, world=W, iface=iface[8 * r:8 * r + 8])
+                    s.dist_solve(a, b, c, d, x, m=m, rank=r, world=W, iface_all=iface)
+                res.setdefault(f"rank{r}", []).append(timed(one))
+        out["rounds_ms"] = {k: [round(t, 4) for t in v] for k, v in res.items()}
+    if args.ab:
+        from paper_2501_05938_b200.solver import PM_OPT_UPPER_FUSED
+
+        res = {}
+        for _ in range(args.ab):
+            for fused in (2, 1, 0):
+                s.set_option(PM_OPT_UPPER_FUSED, fused)
+                res.setdefault(f"single_f{fused}", []).append(timed(lambda: s.solve_device(a, b, c, d, m=m, out=x)))
+                for r in (0, W - 1):
+                    def one():
+                        s.dist_reduce(a, b, c, d, m=m, rank=r, world=W, iface=iface[8 * r:8 * r + 8])
+                        s.dist_solve(a, b, c, d, x, m=m, rank=r, world=W, iface_all=iface)
+                    res.setdefault(f"rank{r}_f{fused}", []).append(timed(one))
+        s.set_option(PM_OPT_UPPER_FUSED, 1)
+        import statistics
+
+        out["ab_median_ms"] = {k: round(statistics.median(v), 4) for k, v in res.items()}
+        out["ab_all_ms"] = {k: [round(t, 4) for t in v] for k, v in res.items()}
     s.check()
     print(json.dumps(out))
 
