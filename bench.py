@@ -467,7 +467,7 @@ def check_rank(ctx, x_local, n_total: int, row0: int, seed: int) -> dict:
 
 
 def solve_phase(ctx, args, solver, n_total: int, exchange: str, timed_steps: int, want_e2e: bool,
-                want_check: bool, time_both_exchanges: bool):
+                want_check: bool, time_both_exchanges: bool, idle_probe: bool = False):
     """Generate this rank's rows of an n_total-row system, time `timed_steps`
     device-resident solves (+ per-kernel event times), optionally the other
     exchange, the oracle check and the e2e solves.  Returns a dict (per rank;
@@ -527,6 +527,24 @@ def solve_phase(ctx, args, solver, n_total: int, exchange: str, timed_steps: int
         return ctx.max(e0.elapsed_time(e1)), clk.summary()
 
     fn = step_fn(main_ex)
+    idle_ms = None
+    if idle_probe:
+        # one solve from an idle GPU (after the warm-up solves and 1 s of
+        # idle): B200 holds its burst clocks for ~40-50 ms of back-to-back
+        # solves, then its power limit takes ~10 % (tools/power_probe.py)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                fn()
+        torch.cuda.synchronize()
+        time.sleep(1.0)
+        ctx.barrier()
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            i0.record(stream)
+            fn()
+            i1.record(stream)
+        torch.cuda.synchronize()
+        idle_ms = ctx.max(i0.elapsed_time(i1))
     ms, clocks = timed(fn, timed_steps)
     launches = (dsolvers[main_ex].last_launches if main_ex else solver.last_launch_count)
     # per-kernel CUDA-event times (same steps again, events bracketing every
@@ -540,7 +558,7 @@ def solve_phase(ctx, args, solver, n_total: int, exchange: str, timed_steps: int
     ktimes = solver.kernel_times()
     solver.set_option(PM_OPT_KERNEL_TIMES, 0)
     solver.check()
-    out = {"ms": ms, "ms_per_step": ms / timed_steps, "clocks": clocks, "ktimes": ktimes,
+    out = {"ms": ms, "ms_per_step": ms / timed_steps, "clocks": clocks, "ktimes": ktimes, "idle_ms": idle_ms,
            "launches_per_step": launches, "n_loc": n_loc, "row0": row0, "rows": rows, "exchange": main_ex}
     if world > 1:
         ex = {main_ex: {"ms_per_step": ms / timed_steps, "value": n_total * timed_steps / (ms / 1e3)}}
@@ -830,7 +848,7 @@ def run_single(args, ctx):
         # config 5 beside the metric line: 1e9 rows over the same ranks
         n5 = int(args.c5_rows)
         r5 = solve_phase(ctx, args, solver, n5, args.exchange, args.steps, want_e2e=False, want_check=True,
-                         time_both_exchanges=True)
+                         time_both_exchanges=True, idle_probe=True)
         rf5 = roofline(r5, esz)
         c5 = {"workload": f"one FP64 SLAE, N={n5:.3g} rows in total, m={args.m} (BASELINE config 5), "
                           f"row-sharded over {world} rank(s) (strong scaling)",
@@ -839,7 +857,12 @@ def run_single(args, ctx):
               **({"exchanges": r5["exchanges"]} if "exchanges" in r5 else {}),
               "whole_solve_frac": rf5["whole_solve"]["frac"], "stage3_frac": rf5["frac"],
               "stage1_frac": rf5["stage1"]["frac"], "kernels_ms": rf5["kernels_ms"],
-              "gpu_launches_per_step": r5["launches_per_step"], "check": r5["check"], "clocks": r5["clocks"]}
+              "gpu_launches_per_step": r5["launches_per_step"], "check": r5["check"], "clocks": r5["clocks"],
+              "idle_solve": {"ms": r5["idle_ms"],
+                             "whole_solve_frac": rf5["whole_solve"]["bytes_per_unknown"] * n5 / max(1, world)
+                             / (r5["idle_ms"] / 1e3) / 1e9 / rf5["peak"] if r5["idle_ms"] else None,
+                             "note": "one solve after 1 s idle (burst clocks); the timed steps run back to back "
+                                     "for ~0.3 s, under the power limit (sw_power_cap)"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.precision == "f64":

@@ -133,7 +133,11 @@ typedef struct pm_model_bundle {
                                   node-ring lines from L2 instead of writing them
                                   back; bit 1 sets L2 eviction priorities on its
                                   bulk copies (Stage-1 reads evict_last, Stage-3
-                                  re-reads and x stores evict_first); default 3  */
+                                  re-reads and x stores evict_first); bit 2 (one
+                                  stage per warp) issues the next tile's copies
+                                  inside the current job; bit 3 lets the control
+                                  warp publish ready segments out of round order;
+                                  default 15                                      */
 #define PM_OPT_BATCH_STATS 27  /* tile-stream kernel: accumulate clock64 wait /
                                   work counters (pm_batch_stream_stats; off)      */
 #define PM_OPT_PAIR_TILES 19   /* level-0 pair tiles (two m-blocks per lane, 64*m

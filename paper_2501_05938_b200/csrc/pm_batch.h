@@ -71,6 +71,8 @@ struct StreamArgs {
   int* flag = nullptr;
   int discard = 1;  // discard.global.L2 on consumed node-ring lines
   int hints = 1;    // L2 eviction priorities on the bulk copies
+  int early = 0;    // one stage per warp: issue the next tile's copies inside the current job
+  int ooo = 0;      // control warp publishes ready segments out of round order
   unsigned long long* stats = nullptr;  // [15] diagnostics (PM_OPT_BATCH_STATS) or null
   unsigned long long* tl = nullptr;     // [5][batch] per-system timeline (with stats)
 };

@@ -283,19 +283,47 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
   int jq0 = 0, jq1 = 0;   // the job codes (2 r + solve) in stages 0 / 1
   const uint64_t pol_last = policy_evict_last();
   const uint64_t pol_first = policy_evict_first();
-  auto issue = [&](int s) {  // lane 0
+  // issue_rows decides the next job, arms its stage and copies its rows;
+  // issue_nodes copies a Stage-3 job's tree nodes (after the completion wait
+  // that orders them behind their Stage-1 store).  In early mode (one stage
+  // per warp, A.early) they run inside the current job: the rows as soon as
+  // the current job has consumed its own (after the block sweeps), the nodes
+  // once the stage's node area is free.
+  int pend = -1;  // code of a C job whose node copy is still to issue
+  // per job parity (the job issued next never overwrites the one running):
+  // a C job's values fetched at issue
+  int n_iss = 0;
+  bool pre0 = false, pre1 = false;
+  double2 pv0 = make_double2(0.0, 0.0), pv1 = make_double2(0.0, 0.0);
+  unsigned po0 = 0, po1 = 0;
+  auto issue_rows = [&](int s) {  // lane 0
     const int lag = a_iss - c_iss;
     const bool doA = a_iss < R && (lag < Lmin || (lag < Lmax && !c_ready));
     const int r = doA ? a_iss++ : c_iss++;
-    if (!doA) {
-      c_ready = 0;
-      if (a_iss < R) bulk_wait_complete1();  // A(r) processed >= 1 job ago
-      else bulk_wait0();                     // the tail: A(r) may be the last job
-    }
     const int code = 2 * r + (doA ? 0 : 1);
     if (s == 0) jq0 = code;
     else jq1 = code;
     const Geo g = geo_of(A, r, gw);
+    if (!doA) {
+      // a C whose system's flag was already seen: its boundary values and
+      // Stage-3 count are fetched now, not at the job's start.  The flag was
+      // read relaxed (an acquire load stalls the warp ~0.7 us per job: 19 %
+      // of the kernel when every job prefetched that way); the txy load is
+      // issued only once the flag value is known (control dependency) and
+      // reads L2, where the Stage-2 warp's values landed before its flag
+      // (__threadfence + st.release).
+      const bool pre = c_ready != 0;
+      double2 pv = make_double2(0.0, 0.0);
+      unsigned po = 0;
+      if (pre) {
+        pv = __ldcg(txy_ring(A) + g.slot);
+        po = atomicAdd(A.cnt3 + kCS * g.sys, 1u);
+      }
+      if ((n_iss & 1) == 0) { pre0 = pre; pv0 = pv; po0 = po; }
+      else { pre1 = pre; pv1 = pv; po1 = po; }
+      c_ready = 0;
+    }
+    ++n_iss;
     const int64_t off = (int64_t)g.sys * A.n_sys + (int64_t)g.t * T;
     const uint32_t bytes = static_cast<uint32_t>(g.valid) * sizeof(double);  // valid is even
     fence_proxy_async();
@@ -307,21 +335,35 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
       bulk_g2s_hint(st + T, A.b + off, bytes, &bars[s], pol);
       bulk_g2s_hint(st + 2 * T, A.c + off, bytes, &bars[s], pol);
       bulk_g2s_hint(st + 3 * T, A.d + off, bytes, &bars[s], pol);
-      if (!doA) bulk_g2s_hint(tree(s), A.nodes + g.slot * kNodeBytes, kNodeCopy, &bars[s], pol_first);
     } else {
       bulk_g2s(st, A.a + off, bytes, &bars[s]);
       bulk_g2s(st + T, A.b + off, bytes, &bars[s]);
       bulk_g2s(st + 2 * T, A.c + off, bytes, &bars[s]);
       bulk_g2s(st + 3 * T, A.d + off, bytes, &bars[s]);
-      if (!doA) bulk_g2s(tree(s), A.nodes + g.slot * kNodeBytes, kNodeCopy, &bars[s]);
     }
+    pend = doA ? -1 : code;
   };
+  auto issue_nodes = [&](int s) {  // lane 0
+    if (pend < 0) return;
+    const Geo g = geo_of(A, pend >> 1, gw);
+    pend = -1;
+    if (a_iss < R) bulk_wait_complete1();  // its A processed >= 1 job ago
+    else bulk_wait0();                     // the tail: its A may be the last job
+    if (A.hints) bulk_g2s_hint(tree(s), A.nodes + g.slot * kNodeBytes, kNodeCopy, &bars[s], pol_first);
+    else bulk_g2s(tree(s), A.nodes + g.slot * kNodeBytes, kNodeCopy, &bars[s]);
+  };
+  auto issue = [&](int s) {
+    issue_rows(s);
+    issue_nodes(s);
+  };
+  const bool early = (S == 1) && A.early;
 
   if (lane == 0)
     for (int s = 0; s < S && s < njobs; ++s) issue(s);
 
   Stats st{};
   const long long t_begin = clk();
+  const unsigned long long g_begin = A.tl ? gtimer() : 0ull;
   int na = 0;  // A jobs published so far (mailbox cursor)
   unsigned long long st_a_cyc = 0, st_c_cyc = 0, st_ai_cyc = 0, st_ci_cyc = 0;
   // job trace of 8 sample warps (diagnostics): [code, start, stage ready, end]
@@ -331,7 +373,9 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
     for (int i = 0; i < 8; ++i)
       if (gw == tw[i] && tw[i] < A.nw) trace = A.tl + 5 * A.batch + (size_t)i * 2400 * 4;
   }
+  unsigned long long st_top_cyc = 0, st_top1_cyc = 0;
   for (int k = 0; k < njobs; ++k) {
+    const long long c_top = clk();
     const int s = (S == 2) ? (k & 1) : 0;  // S is 1 or 2 (plan)
     const int code = __shfl_sync(0xffffffffu, s == 0 ? jq0 : jq1, 0);
     const Job j{(code & 1) != 0, code >> 1};
@@ -366,7 +410,19 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
       trace[4 * k] = (unsigned long long)code;
       trace[4 * k + 1] = gtimer();
     }
-    if (j.solve) {
+    const long long c_mid = clk();
+    st_top1_cyc += c_mid - c_top;
+    const unsigned prefetched = __shfl_sync(0xffffffffu, (lane == 0 && j.solve) ? ((k & 1) == 0 ? pre0 : pre1) : 0u, 0);
+    if (j.solve && prefetched) {
+      if (lane == 0) {
+        const double2 v = ((k & 1) == 0) ? pv0 : pv1;
+        xf = v.x;
+        xl = v.y;
+        // c_old is taken from po0/po1 at the end of the job: reading the
+        // atomic's result here would expose its latency (the system's
+        // counter is hit by every warp working on it)
+      }
+    } else if (j.solve) {
       if (A.tl && lane == 0) atomicMin(A.tl + 4 * A.batch + g.sys, (unsigned long long)gtimer());
       // Warp-uniform wait (lane 0 polls, the result is broadcast: the loop is
       // provably convergent, so the shuffle trees below stay plain SHFL):
@@ -396,6 +452,7 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
         c_old = atomicAdd(A.cnt3 + kCS * g.sys, 1u);  // result used at the end of the job
       }
     }
+    st_top_cyc += clk() - c_mid;
     {
       const long long c0 = clk();
       mbar_wait(&bars[s], static_cast<uint32_t>((S == 2 ? (k >> 1) : k) & 1));
@@ -412,6 +469,10 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
     if (!j.solve) {
       // ---- A: Stage 1 of the tile -------------------------------------------
       const Seg seg = block_reduce_fast<M, false>(pa, bad);
+      if (early) {
+        __syncwarp();  // every lane has consumed its rows
+        if (lane == 0 && k + 1 < njobs) issue_rows(s);
+      }
       const Seg top = warp_upsweep(seg, nodes, lane, nblk, bad);
       fence_proxy_async();  // the lanes' node writes -> visible to the bulk store
       __syncwarp();
@@ -419,6 +480,10 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
         if (A.hints) bulk_s2g_hint(A.nodes + g.slot * kNodeBytes, nodes, kNodeCopy, pol_last);
         else bulk_s2g(A.nodes + g.slot * kNodeBytes, nodes, kNodeCopy);
         bulk_commit();
+        if (early && pend >= 0) {
+          bulk_wait_read0();  // the node store has read the node area
+          issue_nodes(s);
+        }
         const int q = static_cast<int>(na % kMbox);
         const long long c0 = clk();
         mbar_wait(&mempty[q], static_cast<uint32_t>(((na / kMbox) & 1) ^ 1));
@@ -439,6 +504,33 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
       block_solve_pairs<M>(pa, xf, xl, xv, bad);
       __syncwarp();
       bad |= !all_finite<M>(xv);
+      if (early) {
+        // rows and nodes consumed: the next job's copies go out now, x leaves
+        // from registers (16-byte stores; the stage is being refilled)
+        if (lane == 0 && k + 1 < njobs) {
+          issue_rows(s);
+          issue_nodes(s);
+        }
+        double* gx = A.x + off + ctx.row0 + r0;
+        if (r0 + M <= g.valid) {
+          if constexpr ((M % 2) == 0) {
+#pragma unroll
+            for (int i = 0; i < M / 2; ++i)
+              __stcs(reinterpret_cast<double2*>(gx) + i, make_double2(xv[2 * i], xv[2 * i + 1]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < M; ++i) __stcs(gx + i, xv[i]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < M; ++i)
+            if (r0 + i < g.valid) __stcs(gx + i, xv[i]);
+        }
+        if (lane == 0 && (prefetched ? ((k & 1) == 0 ? po0 : po1) : c_old) == static_cast<unsigned>(A.tps) - 1) {  // the system's last Stage-3 tile
+          A.cnt3[kCS * g.sys] = 0;
+          *cflag = 0;
+        }
+      } else {
       if constexpr ((M % 2) == 0) {
 #pragma unroll
         for (int i = 0; i < M / 2; ++i)
@@ -455,16 +547,17 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
         else
           bulk_s2g(A.x + off + ctx.row0, sb, static_cast<uint32_t>(g.valid) * sizeof(double));
         bulk_commit();
-        if (c_old == static_cast<unsigned>(A.tps) - 1) {  // the system's last Stage-3 tile
+        if ((prefetched ? ((k & 1) == 0 ? po0 : po1) : c_old) == static_cast<unsigned>(A.tps) - 1) {  // the system's last Stage-3 tile
           A.cnt3[kCS * g.sys] = 0;
           *cflag = 0;
         }
+      }
       }
     }
     __syncwarp();
     const long long c_iss0 = clk();
     (j.solve ? st_c_cyc : st_a_cyc) += c_iss0 - c_job;
-    if (lane == 0 && k + S < njobs) {
+    if (!early && lane == 0 && k + S < njobs) {
       bulk_wait_read0();  // the bulk store has read the stage
       issue(s);
     }
@@ -474,7 +567,7 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
   if (lane == 0) bulk_wait0();
   st.v[9] = clk() - t_begin;
   if (A.tl && lane == 0 && gw < 4096) {  // per-warp summary: A cycles, C cycles, C wait cycles, SM id
-    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)gw * 8;
+    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)gw * 12;
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     sm[0] = st_a_cyc;
@@ -485,6 +578,10 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
     sm[5] = st_ci_cyc;
     sm[6] = st.v[2];
     sm[7] = st.v[3];
+    sm[8] = st.v[9];
+    sm[9] = st_top1_cyc;  // loop top up to the Stage-3 flag section
+    sm[10] = gtimer();
+    sm[11] = st_top_cyc;  // the Stage-3 flag section (prefetched values or the wait)
   }
   if (A.stats && lane == 0)
     for (int i = 0; i < 15; ++i)
@@ -604,7 +701,7 @@ __device__ __forceinline__ void solver_warp(const StreamArgs& A, unsigned char* 
     ++st.v[7];
   }
   if (A.tl && lane == 0 && A.W * gridDim.x + blockIdx.x < 4096) {  // per-CTA Stage-2 count and cycles
-    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)(A.W * gridDim.x + blockIdx.x) * 8;
+    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)(A.W * gridDim.x + blockIdx.x) * 12;
     sm[0] = st.v[7];
     sm[1] = st.v[6];
   }
@@ -632,7 +729,42 @@ __device__ __forceinline__ void control_warp(const StreamArgs& A, unsigned char*
   Stats st{};
   const long long t_begin = clk();
   unsigned long long* ctr = (A.tl && blockIdx.x == 0) ? A.tl + 5 * A.batch + 8 * 2400 * 4 : nullptr;
-  for (int c = 0; c < Rmax; ++c) {
+  if (A.ooo) {
+    // Out of order: publish whatever segments the CTA's warps have ready,
+    // each warp's in its own round order, instead of a whole round at a time
+    // (a round waits for the CTA's slowest warp; its systems complete late).
+    int head = 0;
+    while (__any_sync(0xffffffffu, head < R)) {
+      ++st.v[4];
+      const int q = head % kMbox;
+      const bool ready = head < R && mbar_test(&mfull[q], static_cast<uint32_t>((head / kMbox) & 1));
+      if (!__any_sync(0xffffffffu, ready)) {
+        ++st.v[5];
+        __nanosleep(64);
+        continue;
+      }
+      long long sys = -1 - lane;  // unique key for lanes with nothing to publish
+      if (ready) {
+        const Seg sg = mbox[q];
+        mbar_arrive(&mempty[q]);
+        seg_ring(A)[ring_slot(A, head, gw)] = sg;
+        sys = fdiv(static_cast<uint32_t>(head) * A.nw + gw, A.mg_tps);
+        ++head;
+      }
+      const long long c0 = clk();
+      __syncwarp();
+      __threadfence();  // release: the segments stored above, before the counts
+      const unsigned grp = __match_any_sync(0xffffffffu, sys);
+      if (ready && (__ffs(grp) - 1) == lane) {
+        const unsigned n = __popc(grp);
+        const unsigned old = atomicAdd(A.cnt1 + kCS * sys, n);
+        if (A.tl && old + n == static_cast<unsigned>(A.tps)) A.tl[2 * A.batch + sys] = gtimer();
+      }
+      __syncwarp();
+      st.v[8] += clk() - c0;
+    }
+  }
+  for (int c = 0; !A.ooo && c < Rmax; ++c) {
     ++st.v[4];
     if (ctr && lane == 0 && c < 1200) ctr[2 * c] = gtimer();
     const bool active = c < R;
@@ -660,7 +792,7 @@ __device__ __forceinline__ void control_warp(const StreamArgs& A, unsigned char*
   }
   st.v[10] = clk() - t_begin;
   if (A.tl && lane == 0 && A.W * gridDim.x + blockIdx.x < 4096) {
-    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)(A.W * gridDim.x + blockIdx.x) * 8;
+    unsigned long long* sm = A.tl + 5 * A.batch + 8 * 2400 * 4 + 1200 * 2 + (size_t)(A.W * gridDim.x + blockIdx.x) * 12;
     sm[2] = st.v[8];
     sm[3] = st.v[10];
   }

@@ -174,7 +174,7 @@ struct pm_handle_s {
   pm::BatchPlan last_batch_plan{0, 0, 0, 0, 0, 0};
   // tile-stream batch kernel (PM_OPT_BATCH_CLUSTER = 2)
   int batch_lag = 0;       // PM_OPT_BATCH_LAG (0 = plan)
-  int batch_discard = 3;   // PM_OPT_BATCH_DISCARD: bit 0 discard, bit 1 L2 hints
+  int batch_discard = 15;  // PM_OPT_BATCH_DISCARD: bit 0 discard, 1 L2 hints, 2 early issue, 3 out-of-order publish
   char* bscr = nullptr;    // node / segment / boundary-value rings
   size_t bscr_bytes = 0;
   char* bcnt = nullptr;    // per-system counters and flags, zero between launches
@@ -988,9 +988,11 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
     A.flag = h->dflag;
     A.discard = h->batch_discard & 1;
     A.hints = (h->batch_discard >> 1) & 1;
+    A.early = (h->batch_discard >> 2) & 1;
+    A.ooo = (h->batch_discard >> 3) & 1;
     if (h->batch_stats) {
       // counters + per-system timeline + job traces of 8 warps + control trace of CTA 0
-      const size_t words = 16 + 5 * (size_t)batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8;
+      const size_t words = 16 + 5 * (size_t)batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 12;
       if (words > h->dstats_words) {
         if (h->dstats) cudaFree(h->dstats);
         h->dstats = nullptr;
@@ -1000,7 +1002,7 @@ int solve_batch_impl(pm_handle_t h, const R* a, const R* b, const R* c,
       PM_CUDA(h, cudaMemsetAsync(h->dstats, 0, 16 * sizeof(unsigned long long), st));
       PM_CUDA(h, cudaMemsetAsync(h->dstats + 16, 0xff, 5 * (size_t)batch * sizeof(unsigned long long), st));
       PM_CUDA(h, cudaMemsetAsync(h->dstats + 16 + batch, 0, (size_t)batch * sizeof(unsigned long long), st));
-      PM_CUDA(h, cudaMemsetAsync(h->dstats + 16 + 5 * batch, 0, (8 * 2400 * 4 + 1200 * 2 + 4096 * 8) * sizeof(unsigned long long), st));
+      PM_CUDA(h, cudaMemsetAsync(h->dstats + 16 + 5 * batch, 0, (8 * 2400 * 4 + 1200 * 2 + 4096 * 12) * sizeof(unsigned long long), st));
       A.stats = h->dstats;
       A.tl = h->dstats + 16;
       h->dstats_batch = batch;
@@ -1654,7 +1656,7 @@ int pm_set_option(pm_handle_t h, int option, int64_t value) {
       h->batch_lag = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_DISCARD:
-      if (value < 0 || value > 3) return fail(h, PM_ERR_VALIDATION, "batch discard must lie in [0, 3]");
+      if (value < 0 || value > 15) return fail(h, PM_ERR_VALIDATION, "batch discard must lie in [0, 15]");
       h->batch_discard = (int)value;
       return PM_OK;
     case PM_OPT_BATCH_STATS:
@@ -1758,7 +1760,7 @@ int pm_batch_stream_stats(pm_handle_t h, uint64_t* out15) {
 int pm_batch_stream_timeline(pm_handle_t h, uint64_t* out, int64_t n) {
   if (!h || !out || n < 0) return PM_ERR_VALIDATION;
   std::memset(out, 0, (size_t)n * sizeof(uint64_t));
-  const int64_t have = 5 * h->dstats_batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8;
+  const int64_t have = 5 * h->dstats_batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 12;
   if (n > have) n = have;
   if (!h->dstats || n == 0) return PM_OK;
   PM_CUDA(h, cudaSetDevice(h->device));

@@ -185,7 +185,7 @@ class PartitionSolver:
         wait start)."""
         import numpy as np
 
-        out = np.zeros(5 * batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8, dtype=np.uint64)
+        out = np.zeros(5 * batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 12, dtype=np.uint64)
         self._ok(self._L.pm_batch_stream_timeline(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
                                                   C.c_int64(out.size)))
         return out[:5 * batch].reshape(5, batch)
@@ -195,13 +195,13 @@ class PartitionSolver:
         stage ready, end) and the control-warp iterations of CTA 0 ([1200, 2])."""
         import numpy as np
 
-        out = np.zeros(5 * batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 8, dtype=np.uint64)
+        out = np.zeros(5 * batch + 8 * 2400 * 4 + 1200 * 2 + 4096 * 12, dtype=np.uint64)
         self._ok(self._L.pm_batch_stream_timeline(self._h, out.ctypes.data_as(C.POINTER(C.c_uint64)),
                                                   C.c_int64(out.size)))
         o = 5 * batch
         o2 = o + 8 * 2400 * 4 + 1200 * 2
         return (out[o:o + 8 * 2400 * 4].reshape(8, 2400, 4), out[o + 8 * 2400 * 4:o2].reshape(1200, 2),
-                out[o2:].reshape(4096, 8))
+                out[o2:].reshape(4096, 12))
 
     def last_plan(self) -> list[int]:
         buf = (C.c_int64 * 16)()

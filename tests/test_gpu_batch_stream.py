@@ -28,7 +28,7 @@ def _opts(solver, **kw):
 
 
 def _reset(solver):
-    _opts(solver, kernel=0, ctas=0, warps=0, stages=0, lag=0, discard=3)
+    _opts(solver, kernel=0, ctas=0, warps=0, stages=0, lag=0, discard=15)
 
 
 def _solve(solver, cat, nps, m, out=None, **kw):
@@ -67,8 +67,10 @@ def test_stream_kernel_parity(solver, nps, batch, m, ctas, warps, lag):
 
 
 @pytest.mark.parametrize("stages", [1, 2])
-@pytest.mark.parametrize("discard", [0, 1, 2, 3])
+@pytest.mark.parametrize("discard", list(range(16)))
 def test_stream_kernel_stages_discard(solver, stages, discard):
+    """Option bits: 1 discard consumed node lines, 2 L2 hints, 4 early issue
+    (one stage per warp), 8 out-of-order publication by the control warp."""
     nps, batch, m = 12_000, 40, 10
     systems, cat = _batch_systems(nps, batch, 5 + stages)
     x, plan = _solve(solver, cat, nps, m, ctas=5, warps=6, stages=stages, discard=discard)
