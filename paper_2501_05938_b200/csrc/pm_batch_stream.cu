@@ -306,16 +306,17 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
     const Geo g = geo_of(A, r, gw);
     if (!doA) {
       // a C whose system's flag was already seen: its boundary values and
-      // Stage-3 count are fetched now, not at the job's start.  The flag was
-      // read relaxed (an acquire load stalls the warp ~0.7 us per job: 19 %
-      // of the kernel when every job prefetched that way); the txy load is
-      // issued only once the flag value is known (control dependency) and
-      // reads L2, where the Stage-2 warp's values landed before its flag
-      // (__threadfence + st.release).
+      // Stage-3 count are fetched now, not at the job's start.  The job-top
+      // prefetch reads the flag relaxed (an acquire there stalls the warp
+      // ~0.7 us on every job: 19 % of the kernel); the acquire re-read here,
+      // only for a C about to use the values, orders the txy load behind the
+      // Stage-2 warp's release.  It cannot see the flag cleared: the last
+      // Stage-3 tile of the system clears it, and this one has not counted.
       const bool pre = c_ready != 0;
       double2 pv = make_double2(0.0, 0.0);
       unsigned po = 0;
       if (pre) {
+        (void)ld_acquire_u32(A.sflag + kCS * g.sys);
         pv = __ldcg(txy_ring(A) + g.slot);
         po = atomicAdd(A.cnt3 + kCS * g.sys, 1u);
       }

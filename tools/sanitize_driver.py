@@ -48,8 +48,12 @@ def main():
     nps, batch = 4_000, 6
     a, b, c, d = oracle.generate(nps * batch, 2)
     t = [torch.from_numpy(v).cuda() for v in (a, b, c, d)]
-    for cl in (0, 1):
+    from paper_2501_05938_b200.solver import PM_OPT_BATCH_WARPS, PM_OPT_MAX_CTAS, PM_OPT_UPPER_FUSED
+
+    for cl in (0, 1, 2):  # level kernels, cluster kernel, tile-stream kernel (small grid: many rounds)
         s.set_option(PM_OPT_BATCH_CLUSTER, cl)
+        s.set_option(PM_OPT_MAX_CTAS, 4 if cl == 2 else 0)
+        s.set_option(PM_OPT_BATCH_WARPS, 4 if cl == 2 else 0)
         xb = s.solve_batch_device(*t, n_per_system=nps, m=10).cpu().numpy()
         s.check()
         for k in range(batch):
@@ -58,17 +62,45 @@ def main():
             sa[0] = 0.0
             sc[-1] = 0.0
             check(xb[sl], sa, b[sl].copy(), sc, d[sl].copy())
+        if cl == 2:
+            assert s.last_batch_plan()["kernel"] == "stream", s.last_batch_plan()
     s.set_option(PM_OPT_BATCH_CLUSTER, 0)
-    # row-sharded, two virtual ranks with the P2P exchange
-    n, world = 50_000, 2
+    s.set_option(PM_OPT_MAX_CTAS, 0)
+    s.set_option(PM_OPT_BATCH_WARPS, 0)
+    # row-sharded, two virtual ranks with the P2P exchange; then the fused
+    # upper levels for ranks (PM_OPT_UPPER_FUSED = 2) at a size where they apply
+    run_p2p(s, 50_000, 3)
+    s.set_option(PM_OPT_UPPER_FUSED, 2)
+    run_p2p(s, 2 * 409_600, 4)
+    s.set_option(PM_OPT_UPPER_FUSED, 1)
+    s.close()
+    print("sanitize driver ok")
+
+
+def run_p2p(s, n, seed):
+    import torch
+
+    import oracle
+    from paper_2501_05938_b200 import PartitionSolver
+
+    def check(x, a, b, c, d, tol=1e-10):
+        e = oracle.rel_err(np.ascontiguousarray(x, np.float64), oracle.thomas(a, b, c, d))
+        assert e <= tol, e
+
+    world = 2
+    a, b, c, d = oracle.generate(n, seed)
     a, b, c, d = oracle.generate(n, 3)
     other = PartitionSolver(0)
+    from paper_2501_05938_b200.solver import PM_OPT_UPPER_FUSED
+
+    other.set_option(PM_OPT_UPPER_FUSED, 2)
     hs = [s, other]
     bufs = [h.dist_exchange_alloc(world) for h in hs]
     for r, h in enumerate(hs):
         h.dist_set_peers(bufs, r)
-    rows = [25_000, 25_000]
-    loc = [[torch.from_numpy(v[r * 25_000:(r + 1) * 25_000].copy()).cuda() for v in (a, b, c, d)]
+    half = n // 2
+    rows = [half, n - half]
+    loc = [[torch.from_numpy(v[r * half:r * half + rows[r]].copy()).cuda() for v in (a, b, c, d)]
            for r in range(world)]
     for r in range(world):
         hs[r].dist_reduce_p2p(*loc[r], m=10)
@@ -81,8 +113,6 @@ def main():
         h.check()
     check(torch.cat(xs).cpu().numpy(), a, b, c, d)
     other.close()
-    s.close()
-    print("sanitize driver ok")
 
 
 if __name__ == "__main__":
