@@ -770,7 +770,7 @@ def run_batch(args, ctx):
                                      "with copy-out)",
                    "steps": args.e2e_steps,
                    "timing": "host wall clock around pm_solve_batch_host_f64 (3 streams, chunks of "
-                             "~64 MB), median, max over ranks"}
+                             "~256 MB), median, max over ranks"}
     value = n_total * args.steps / (ms / 1e3)
     peak, peak_src = peaks()
     if plan["kernel"] in ("cluster", "stream"):

@@ -193,7 +193,7 @@ int pm_batch_stream_counters(pm_handle_t h, uint32_t* out, int64_t n);
 int pm_batch_stream_timeline(pm_handle_t h, uint64_t* out, int64_t n);
 
 /* Batch of independent systems from host memory, end to end (config 4):
- * chunks of `systems_per_chunk` systems (0 = ~64 MB of inputs per chunk) flow
+ * chunks of `systems_per_chunk` systems (0 = ~256 MB of inputs per chunk) flow
  * H2D -> batch solve -> D2H through a ring of `depth` device staging slots
  * (0 = 3) on separate copy-in / compute / copy-out streams, so the copy-in of
  * one chunk overlaps the copy-out of an earlier one (PCIe is full duplex).

@@ -1350,8 +1350,11 @@ int solve_batch_host_impl(pm_handle_t h, const R* a, const R* b, const R* c, con
   if (r) return r;
   if (depth == 0) depth = 3;
   if (depth < 1 || depth > 32) return fail(h, PM_ERR_VALIDATION, "depth must lie in [1, 32] (0 = 3)");
-  if (systems_per_chunk <= 0)  // ~64 MB of a, b, c, d per chunk
-    systems_per_chunk = std::max<int64_t>(1, ((int64_t)64 << 20) / (4 * (int64_t)sizeof(R) * n_per_system));
+  // ~256 MB of a, b, c, d per chunk: config 4 end to end 255.6 ms with 64 MB
+  // chunks, 246 ms from 256 MB up (0.96-0.97 of the pinned H2D bound;
+  // tools/batch_host_probe.py, profiles/round2/batch_host_probe.json)
+  if (systems_per_chunk <= 0)
+    systems_per_chunk = std::max<int64_t>(1, ((int64_t)256 << 20) / (4 * (int64_t)sizeof(R) * n_per_system));
   systems_per_chunk = std::min<int64_t>(systems_per_chunk, batch);
   const int64_t nchunks = (batch + systems_per_chunk - 1) / systems_per_chunk;
   depth = (int)std::min<int64_t>(depth, nchunks);
