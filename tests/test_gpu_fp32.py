@@ -120,15 +120,21 @@ def test_f32_batch(solver, nps, batch, m):
         _check32(x[k * nps:(k + 1) * nps], *s)
 
 
+@pytest.mark.parametrize("fused", [1, 2])
 @pytest.mark.parametrize("world", [2, 3])
-def test_f32_dist_virtual_ranks(solver, world):
+def test_f32_dist_virtual_ranks(solver, world, fused):
+    """fused = 2: the ranks' upper levels in two launches where they apply
+    (PM_OPT_UPPER_FUSED; FP32 level 0 uses pair tiles of 64 m rows)."""
     import torch
 
     from paper_2501_05938_b200 import PartitionSolver
     from paper_2501_05938_b200.dist import split_rows
+    from paper_2501_05938_b200.solver import PM_OPT_UPPER_FUSED
 
-    n, m = 1_000_003, 10
+    n, m = 1_000_003 if fused == 1 else 2_600_007, 10
     handles = [solver] + [PartitionSolver(0) for _ in range(world - 1)]
+    for h in handles:
+        h.set_option(PM_OPT_UPPER_FUSED, fused)
     a, b, c, d = _f32_system(n, 5)
     rows = split_rows(n, world, m)
     offs = np.concatenate([[0], np.cumsum(rows)])
@@ -144,6 +150,7 @@ def test_f32_dist_virtual_ranks(solver, world):
         xs.append(x)
     for h in handles:
         h.check()
+    solver.set_option(PM_OPT_UPPER_FUSED, 1)
     for h in handles[1:]:
         h.close()
     _check32(torch.cat(xs).cpu().numpy(), a, b, c, d)

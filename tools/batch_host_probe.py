@@ -18,10 +18,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
 def main():
-    import numpy as np
     import torch
 
-    import oracle  # noqa: F401  (generator mirror not needed: device generator + copy)
     from paper_2501_05938_b200 import PartitionSolver, pinned_empty
 
     p = argparse.ArgumentParser()
