@@ -1,5 +1,6 @@
 import json, sys
-line = sys.stdin.read().strip().splitlines()
+# usage: summarize_bench.py [BENCH.json]  (stdin when no path is given)
+line = (open(sys.argv[1]).read() if len(sys.argv) > 1 else sys.stdin.read()).strip().splitlines()
 try:
     d = json.loads(line[-1])
 except Exception:

@@ -9,7 +9,7 @@ This tool reads the CSV launch lists written by
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
       --clock-control none --csv --log-file L.csv python bench.py ...
 
-(scripts/gpu_traffic.sh), takes the LAST launch of each kernel of interest
+(scripts/gpu_final_evidence.sh), takes the LAST launch of each kernel of interest
 (the last step: warm caches as in the timed region) and stamps the result
 with the build hash.
 
