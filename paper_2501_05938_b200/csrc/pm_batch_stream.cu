@@ -76,7 +76,6 @@ struct Layout {
   size_t wnode;   // 31 Node: control warp's tree
   size_t chain;   // [tps] Seg: one system's tile segments, chain nodes in place
   size_t gbar;    // mbarrier of the Stage-2 warp's segment gather
-  size_t zbar;    // [W + 1] never-completing mbarriers: timed sleeps of the flag waits
   size_t total;
 };
 
@@ -102,8 +101,6 @@ __host__ __device__ inline Layout stream_layout(int m, int W, int S, int tps) {
   o += (size_t)tps * sizeof(Seg);
   L.gbar = o;
   o += sizeof(uint64_t);
-  L.zbar = o;
-  o += (size_t)(W + 1) * sizeof(uint64_t);
   L.total = align_up(o, 128);
   return L;
 }
@@ -191,22 +188,6 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// A real timed sleep: try_wait on an mbarrier whose phase never completes
-// suspends the warp for up to `ns` (nanosleep may return at once, and a
-// spinning poll would steal the compute warps' issue slots).
-__device__ __forceinline__ uint32_t sleep_on(uint64_t* zbar, uint32_t ns) {
-  uint32_t done;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0, %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(done)
-      : "r"(smem_u32(zbar)), "r"(ns)
-      : "memory");
-  return done;  // always 0: the phase never completes
-}
 // generic-proxy global writes (made visible to this thread by an acquire) ->
 // ordered before this thread's later bulk copies (async proxy)
 __device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
@@ -265,7 +246,6 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
   uint64_t* mfull = reinterpret_cast<uint64_t*>(smem + lay.mfull) + w * kMbox;
   uint64_t* mempty = reinterpret_cast<uint64_t*>(smem + lay.mempty) + w * kMbox;
   Seg* mbox = reinterpret_cast<Seg*>(smem + lay.mbox) + w * kMbox;
-  uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + lay.zbar) + w;
   auto rows = [&](int s) { return reinterpret_cast<double*>(wst + (size_t)s * lay.stage); };
   auto tree = [&](int s) { return reinterpret_cast<Node*>(wst + (size_t)s * lay.stage + 4 * T * sizeof(double)); };
 
@@ -434,9 +414,14 @@ __device__ __forceinline__ void compute_warp(const StreamArgs& A, unsigned char*
         const long long c0 = clk();
         ++st.v[1];
         const uint64_t t0 = gtimer();
+        unsigned backoff = 128;
         while (!ok) {
-          unsigned v = sleep_on(zbar, 1000);
-          v |= (lane == 0) ? ld_relaxed_u32(cflag) : 0u;
+          // exponential nanosleep back-off: the polls (an mbarrier timed
+          // try_wait returns after ~100 ns) were a third of the kernel's
+          // instructions when a system's Stage 2 ran late
+          __nanosleep(backoff);
+          backoff = backoff < 2048 ? 2 * backoff : 2048;
+          unsigned v = (lane == 0) ? ld_relaxed_u32(cflag) : 0u;
           if (lane == 0 && !v && gtimer() - t0 > kStreamWaitNs) {
             atomicOr(A.flag, kFlagTimeout);
             v = 1u;
@@ -670,7 +655,6 @@ __device__ __forceinline__ void system_stage2(const StreamArgs& A, uint32_t s, S
 __device__ __forceinline__ void solver_warp(const StreamArgs& A, unsigned char* smem, const Layout& lay, int lane,
                                             bool& bad) {
   uint64_t* gbar = reinterpret_cast<uint64_t*>(smem + lay.gbar);
-  uint64_t* zbar = reinterpret_cast<uint64_t*>(smem + lay.zbar) + A.W;
   Seg* tsegs = reinterpret_cast<Seg*>(smem + lay.chain);
   Node* wnode = reinterpret_cast<Node*>(smem + lay.wnode);
   uint32_t gphase = 0;
@@ -682,9 +666,11 @@ __device__ __forceinline__ void solver_warp(const StreamArgs& A, unsigned char* 
     ok = __shfl_sync(0xffffffffu, ok, 0);
     if (!ok) {
       const uint64_t t0 = gtimer();
+      unsigned backoff = 256;
       while (!ok) {
-        unsigned v = sleep_on(zbar, 500);
-        v |= (lane == 0) ? (ld_relaxed_u32(cnt) == tps) : 0u;
+        __nanosleep(backoff);
+        backoff = backoff < 2048 ? 2 * backoff : 2048;
+        unsigned v = (lane == 0) ? (ld_relaxed_u32(cnt) == tps) : 0u;
         if (lane == 0 && !v && gtimer() - t0 > kStreamWaitNs) {
           atomicOr(A.flag, kFlagTimeout);
           v = 1u;
@@ -735,15 +721,18 @@ __device__ __forceinline__ void control_warp(const StreamArgs& A, unsigned char*
     // each warp's in its own round order, instead of a whole round at a time
     // (a round waits for the CTA's slowest warp; its systems complete late).
     int head = 0;
+    unsigned idle_ns = 64;
     while (__any_sync(0xffffffffu, head < R)) {
       ++st.v[4];
       const int q = head % kMbox;
       const bool ready = head < R && mbar_test(&mfull[q], static_cast<uint32_t>((head / kMbox) & 1));
       if (!__any_sync(0xffffffffu, ready)) {
         ++st.v[5];
-        __nanosleep(64);
+        __nanosleep(idle_ns);
+        idle_ns = idle_ns < 1024 ? 2 * idle_ns : 1024;
         continue;
       }
+      idle_ns = 64;
       long long sys = -1 - lane;  // unique key for lanes with nothing to publish
       if (ready) {
         const Seg sg = mbox[q];
@@ -818,8 +807,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1) batch_stream_kernel(StreamA
       mbar_init(&e[i], 1);
     }
     mbar_init(reinterpret_cast<uint64_t*>(smem + lay.gbar), 1);
-    uint64_t* zb = reinterpret_cast<uint64_t*>(smem + lay.zbar);
-    for (int i = 0; i <= A.W; ++i) mbar_init(&zb[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
