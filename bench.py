@@ -653,8 +653,10 @@ def roofline(res, esz: int):
     ach_solve = b_solve * n_loc / (t_solve / 1e3) / 1e9
     ach_reduce = b_reduce * n_loc / (t_reduce / 1e3) / 1e9
     whole = b_total * n_loc / (res["ms_per_step"] / 1e3) / 1e9
-    traffic, tprov = traffic_for("solve_level0_bytes_per_launch") if esz == 8 and n_loc == 80_000_000 \
-        else (None, "captured for the N=8e7 FP64 launch only")
+    if n_loc == 80_000_000:
+        traffic, tprov = traffic_for("solve_level0_bytes_per_launch" if esz == 8 else "solve_level0_f32_bytes_per_launch")
+    else:
+        traffic, tprov = None, "captured for the N=8e7 launches (FP64, FP32) only"
     return {"bound": "hbm", "achieved": ach_solve, "peak": peak, "unit": "GB/s", "frac": ach_solve / peak,
             "traffic": traffic, "traffic_source": tprov,
             "kernel": "Stage 3 (SOLVE level 0): %g B/unknown x %d rows per launch" % (b_solve, n_loc),

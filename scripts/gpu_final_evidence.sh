@@ -9,9 +9,11 @@ timeout 600 ncu $M --log-file gpurun_out/launches_single_$TAG.csv python bench.p
 timeout 900 ncu $M --log-file gpurun_out/launches_batch_$TAG.csv python bench.py --workload batch --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_batch_$TAG.log 2>&1; echo "batch rc=$?"
 timeout 900 ncu $M --log-file gpurun_out/launches_cluster_$TAG.csv python bench.py --workload batch --opt batch_cluster=1 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_cluster_$TAG.log 2>&1; echo "cluster rc=$?"
 timeout 900 ncu $M --log-file gpurun_out/launches_stream_$TAG.csv python bench.py --workload batch --opt batch_cluster=2 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_stream_$TAG.log 2>&1; echo "stream rc=$?"
+timeout 600 ncu $M --log-file gpurun_out/launches_f32_$TAG.csv python bench.py --precision f32 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_f32_$TAG.log 2>&1; echo "f32 rc=$?"
 timeout 900 ncu $M --log-file gpurun_out/launches_c5_$TAG.csv python bench.py --workload c5 --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_c5_$TAG.log 2>&1; echo "c5 rc=$?"
 python tools/stamp_traffic.py --single gpurun_out/launches_single_$TAG.csv --batch gpurun_out/launches_batch_$TAG.csv \
   --batch-cluster gpurun_out/launches_cluster_$TAG.csv --batch-stream gpurun_out/launches_stream_$TAG.csv \
+  --f32 gpurun_out/launches_f32_$TAG.csv \
   --out gpurun_out/ncu_traffic_$TAG.json > /dev/null; echo "stamp rc=$?"
 cp gpurun_out/ncu_traffic_$TAG.json profiles/ncu_traffic.json
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:warp_tile_kernel -s 2 -c 2 -o gpurun_out/prof_warp_$TAG python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-c5 > gpurun_out/ncu_warp_$TAG.log 2>&1; echo "full rc=$?"

@@ -67,11 +67,12 @@ def main():
     p.add_argument("--batch", help="launch list of bench.py --workload batch (level kernels)")
     p.add_argument("--batch-cluster", help="launch list of the batch cluster kernel")
     p.add_argument("--batch-stream", help="launch list of the batch tile-stream kernel")
+    p.add_argument("--f32", help="launch list of bench.py --precision f32 (pair-tile kernels)")
     p.add_argument("--out", default=str(ROOT / "profiles" / "ncu_traffic.json"))
     a = p.parse_args()
     doc = {"build_hash": bench.kernel_build_hash(),
            "source": "tools/stamp_traffic.py from ncu launch lists (last launch of each kernel): "
-                     + ", ".join(Path(x).name for x in (a.single, a.batch, a.batch_cluster, a.batch_stream) if x)}
+                     + ", ".join(Path(x).name for x in (a.single, a.batch, a.batch_cluster, a.batch_stream, a.f32) if x)}
     s = per_launch(a.single)
     doc["reduce_level0_bytes_per_launch"] = last_of(s, "warp_tile_kernel<10, 0")
     doc["solve_level0_bytes_per_launch"] = last_of(s, "warp_tile_kernel<10, 1")
@@ -85,6 +86,10 @@ def main():
     if a.batch_stream:
         c = per_launch(a.batch_stream)
         doc["batch_stream_bytes_per_launch"] = last_of(c, "batch_stream")
+    if a.f32:
+        f = per_launch(a.f32)
+        doc["reduce_level0_f32_bytes_per_launch"] = last_of(f, "warp_pair_kernel<10, 0")
+        doc["solve_level0_f32_bytes_per_launch"] = last_of(f, "warp_pair_kernel<10, 1")
     Path(a.out).write_text(json.dumps(doc, indent=1) + "\n")
     print(json.dumps(doc, indent=1))
 
