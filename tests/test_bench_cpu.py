@@ -72,3 +72,29 @@ def test_traffic_is_quoted_only_for_its_build(tmp_path, monkeypatch):
     (tmp_path / "profiles" / "ncu_traffic.json").write_text(json.dumps(doc))
     v, why = bench.traffic_for("solve_level0_bytes_per_launch")
     assert v is None and why.startswith("stale")
+
+
+def test_stamp_traffic_reads_the_committed_launch_lists(tmp_path):
+    """tools/stamp_traffic.py on the committed round-2 launch lists gives the
+    per-launch DRAM bytes of the committed stamp (same capture), and the
+    level-0 traffic is the algorithmic 32 / 40 B per unknown within 1 %."""
+    fin = ROOT / "profiles" / "round2" / "final"
+    out = tmp_path / "t.json"
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "stamp_traffic.py"),
+                        "--single", str(fin / "launches_single_r2h.csv"),
+                        "--batch", str(fin / "launches_batch_r2h.csv"),
+                        "--batch-cluster", str(fin / "launches_cluster_r2h.csv"),
+                        "--batch-stream", str(fin / "launches_stream_r2h.csv"),
+                        "--f32", str(fin / "launches_f32_r2i.csv"), "--out", str(out)],
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    doc = json.loads(out.read_text())
+    ref = json.loads((fin / "ncu_traffic_r2h.json").read_text())
+    for k in ("reduce_level0_bytes_per_launch", "solve_level0_bytes_per_launch",
+              "batch_solve_level0_bytes_per_launch", "batch_stream_bytes_per_launch"):
+        assert doc[k] == ref[k], k
+    n = 80_000_000
+    assert abs(doc["reduce_level0_bytes_per_launch"] / (32 * n) - 1) < 0.01
+    assert abs(doc["solve_level0_bytes_per_launch"] / (40 * n) - 1) < 0.01
+    assert abs(doc["solve_level0_f32_bytes_per_launch"] / (20 * n) - 1) < 0.02
+    assert doc["build_hash"] == bench.kernel_build_hash()
