@@ -134,6 +134,9 @@ def self_launch(args) -> int:
     return subprocess.run(cmd, env=env).returncode
 
 
+SPEC_HBM_GBS = 8000.0  # north_star "about 8 TB/s" (B200_PROFILING.md: 7.7 HGX / 8 DGX)
+
+
 def kernel_build_hash() -> str:
     """Hash of the solver's CUDA sources: ncu traffic figures are only quoted
     for the build they were captured on."""
@@ -664,7 +667,11 @@ def roofline(res, esz: int):
             "stage1": {"achieved": ach_reduce, "frac": ach_reduce / peak, "kernel_ms": t_reduce,
                        "bytes_per_unknown": b_reduce},
             "whole_solve": {"achieved": whole, "frac": whole / peak, "bytes_per_unknown": b_total,
-                            "kernel_ms_sum": sum(t for (_, _, t) in kt) / steps},
+                            "kernel_ms_sum": sum(t for (_, _, t) in kt) / steps,
+                            "frac_of_spec": whole / SPEC_HBM_GBS},
+            "spec": {"hbm_gbs": SPEC_HBM_GBS, "frac": ach_solve / SPEC_HBM_GBS,
+                     "note": "north_star's ~8 TB/s (B200 DGX figure; HGX 7.7 TB/s); frac/peak use the "
+                             "measured copy bandwidth"},
             "kernels_ms": per_kernel}
 
 
