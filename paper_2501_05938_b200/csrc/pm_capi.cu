@@ -471,7 +471,7 @@ int build_plan(pm_handle_t h, int64_t n, int m, const R* a, const R* b, const R*
   if (h->dist_fused) {
     seg2_off = (total + 31) / 32 * 32;
     // segments, chain nodes, boundary pairs | level 2's CTA tree
-    total = seg2_off + (size_t)lv[1].ntiles * 18 + (Prec<R>::dist_tree2_bytes() + 2 * sizeof(R)) / sizeof(R);
+    total = seg2_off + ((size_t)lv[1].ntiles * 18 + 3) / 4 * 4 + (Prec<R>::dist_tree2_bytes() + 2 * sizeof(R)) / sizeof(R);
   }
   int st = ensure_scratch(h, total * sizeof(R));
   if (st) return st;
@@ -683,7 +683,7 @@ int enq_dist_upper(pm_handle_t h, int mode, bool zf, bool zl, int rank, int worl
   u.seg2 = base;
   u.node2 = base + 8 * G;
   u.x2 = base + 16 * G;
-  u.tree2 = base + 18 * G;
+  u.tree2 = base + (18 * G + 3) / 4 * 4;  // 16-byte aligned for both precisions
   u.chain = h->dist_chain;
   u.ragged = L1.pad_mode == 0;
   u.zero_first = zf;

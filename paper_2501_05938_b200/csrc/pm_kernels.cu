@@ -729,15 +729,28 @@ __device__ __forceinline__ Seg dist_level2_up(const DistUpperArgs& u, UpperSmem&
 // REDUCE's last CTA builds it, the SOLVE's CTA 0 splits it.
 size_t dist_tree2_bytes() { return sizeof(TreeSmem) + sizeof(Node) * (kUpperP / 32) * 31; }
 __device__ __forceinline__ void tree2_copy(UpperSmem& sm, real* g, bool to_global) {
-  constexpr int W1 = sizeof(TreeSmem) / 4, W2 = sizeof(Node) * (kUpperP / 32) * 31 / 4;
-  static_assert(sizeof(TreeSmem) % 4 == 0 && (sizeof(Node) * (kUpperP / 32) * 31) % 4 == 0, "word copy");
-  unsigned* t = reinterpret_cast<unsigned*>(&sm.tree[1]);
-  unsigned* w = reinterpret_cast<unsigned*>(&sm.wnodes[1][0]);
-  unsigned* gg = reinterpret_cast<unsigned*>(g);
-  for (int i = threadIdx.x; i < W1 + W2; i += kUpperP) {
-    unsigned* sp = (i < W1) ? t + i : w + (i - W1);
-    if (to_global) gg[i] = *sp;
-    else *sp = __ldcg(gg + i);
+  // 16-byte words, all loads of a thread issued before its stores (one L2
+  // round trip instead of one per word: this copy is on the SOLVE's critical path)
+  constexpr int B1 = sizeof(TreeSmem), B2 = sizeof(Node) * (kUpperP / 32) * 31;
+  static_assert(B1 % 16 == 0 && B2 % 16 == 0, "16-byte copy");
+  constexpr int W1 = B1 / 16, W = (B1 + B2) / 16, PER = (W + kUpperP - 1) / kUpperP;
+  uint4* t = reinterpret_cast<uint4*>(&sm.tree[1]);
+  uint4* w = reinterpret_cast<uint4*>(&sm.wnodes[1][0]);
+  uint4* gg = reinterpret_cast<uint4*>(g);
+  uint4 v[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int i = threadIdx.x + j * kUpperP;
+    if (i < W) v[j] = to_global ? ((i < W1) ? t[i] : w[i - W1]) : __ldcg(gg + i);
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int i = threadIdx.x + j * kUpperP;
+    if (i < W) {
+      if (to_global) gg[i] = v[j];
+      else if (i < W1) t[i] = v[j];
+      else w[i - W1] = v[j];
+    }
   }
 }
 
