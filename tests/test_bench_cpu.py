@@ -81,15 +81,15 @@ def test_stamp_traffic_reads_the_committed_launch_lists(tmp_path):
     fin = ROOT / "profiles" / "round2" / "final"
     out = tmp_path / "t.json"
     r = subprocess.run([sys.executable, str(ROOT / "tools" / "stamp_traffic.py"),
-                        "--single", str(fin / "launches_single_r2h.csv"),
-                        "--batch", str(fin / "launches_batch_r2h.csv"),
-                        "--batch-cluster", str(fin / "launches_cluster_r2h.csv"),
-                        "--batch-stream", str(fin / "launches_stream_r2h.csv"),
-                        "--f32", str(fin / "launches_f32_r2i.csv"), "--out", str(out)],
+                        "--single", str(fin / "launches_single_r2j.csv"),
+                        "--batch", str(fin / "launches_batch_r2j.csv"),
+                        "--batch-cluster", str(fin / "launches_cluster_r2j.csv"),
+                        "--batch-stream", str(fin / "launches_stream_r2j.csv"),
+                        "--f32", str(fin / "launches_f32_r2j.csv"), "--out", str(out)],
                        capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     doc = json.loads(out.read_text())
-    ref = json.loads((fin / "ncu_traffic_r2h.json").read_text())
+    ref = json.loads((fin / "ncu_traffic_r2j.json").read_text())
     for k in ("reduce_level0_bytes_per_launch", "solve_level0_bytes_per_launch",
               "batch_solve_level0_bytes_per_launch", "batch_stream_bytes_per_launch"):
         assert doc[k] == ref[k], k
