@@ -31,6 +31,37 @@ __global__ void read4write1(const double2* __restrict__ a, const double2* __rest
   }
 }
 
+// one buffer read with L2-cached loads (ld.global.cg): repeated passes over a
+// buffer that L2 retains run at L2 bandwidth (tools/l2_probe.py)
+__global__ void read1cg(const double2* __restrict__ a, int64_t n2, double* sink) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = __ldcg(a + i);
+    acc += v.x + v.y;
+  }
+  if (acc == 12345.678) *sink = acc;
+}
+
+extern "C" float l2_probe(const double* a, double* sink, int64_t n, int ctas_per_sm, int threads, int reps) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * ctas_per_sm;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  read1cg<<<grid, threads>>>((const double2*)a, n / 2, sink);  // first pass
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) read1cg<<<grid, threads>>>((const double2*)a, n / 2, sink);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return cudaGetLastError() == cudaSuccess ? ms / reps : -1.f;
+}
+
 extern "C" float bw_probe(int kind, const double* a, const double* b, const double* c, const double* d,
                           double* x, int64_t n, int ctas_per_sm, int threads, int reps) {
   int sms = 0;
